@@ -1,0 +1,62 @@
+# Build recipe for the B200 Richardson-Lucy hot path.
+#
+#   make            -> product library + oracle (+ reference shim when /root/reference exists)
+#   make lib        -> paper_1304_7211_b200/libfdgpu.so   (C ABI, sm_100a CUDA)
+#   make oracle     -> oracle/liboracle.so                  (CPU restatement, test-only)
+#   make ref        -> oracle/_ref/libfdref.so              (the reference itself, test/baseline-only)
+#   make cpptests   -> tests/cpp/dropin_test                (reference-API drop-in harness)
+#
+# Built artefacts are git-ignored but travel to the GPU box with gpurun.
+
+NVCC      ?= nvcc
+HOSTCXX   := g++
+HOSTCC    := gcc
+REF_INC   ?= /root/reference/proj/include
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+PY_NCCL   := $(shell python -c "import nvidia.nccl,os;print(os.path.dirname(nvidia.nccl.__file__))" 2>/dev/null)
+
+PKG       := paper_1304_7211_b200
+LIB       := $(PKG)/libfdgpu.so
+CSRC      := $(wildcard $(PKG)/csrc/*.cu) $(wildcard $(PKG)/csrc/*.cpp)
+CHDR      := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/fdgpu.h
+
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
+             -Iinclude -I$(PKG)/csrc --expt-relaxed-constexpr -Xptxas -warn-spills
+
+ORACLE    := oracle/liboracle.so
+REFLIB    := oracle/_ref/libfdref.so
+DROPIN    := tests/cpp/dropin_test
+
+HAVE_REF  := $(wildcard $(REF_INC)/fastdeconv/rl.hpp)
+
+all: lib oracle $(if $(HAVE_REF),ref cpptests)
+
+lib: $(LIB)
+oracle: $(ORACLE)
+ref: $(REFLIB)
+cpptests: $(DROPIN)
+
+$(LIB): $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC) -lcudart
+
+$(ORACLE): oracle/psf.c oracle/conv.c oracle/rl.c oracle/oracle.h oracle/plan.h
+	$(HOSTCC) -O3 -std=c11 -D_POSIX_C_SOURCE=200809L -fopenmp -ffp-contract=off -fPIC -shared \
+	    -o $@ oracle/psf.c oracle/conv.c oracle/rl.c -lm
+
+$(REFLIB): oracle/ref_shim.cpp oracle/ref_shim.h
+	@mkdir -p oracle/_ref
+	$(HOSTCXX) -std=c++20 -O2 -ffp-contract=off -fPIC -shared -pthread -I$(REF_INC) -Ioracle \
+	    -o $@ oracle/ref_shim.cpp
+
+# The drop-in harness compiles the reference's own image.hpp/psf.hpp (data
+# model) with OUR include/fastdeconv/{convolve,rl}.hpp shadowing the
+# reference's hot-path headers, and links the CUDA library + the oracle.
+$(DROPIN): tests/cpp/dropin_test.cpp include/fastdeconv/convolve.hpp include/fastdeconv/rl.hpp include/fdgpu.h $(LIB) $(ORACLE)
+	$(HOSTCXX) -std=c++20 -O2 -Iinclude -I$(REF_INC) -Ioracle -o $@ tests/cpp/dropin_test.cpp \
+	    -L$(PKG) -lfdgpu -Loracle -loracle -Wl,-rpath,'$$ORIGIN/../../$(PKG)' \
+	    -Wl,-rpath,'$$ORIGIN/../../oracle' -fopenmp
+
+clean:
+	rm -f $(LIB) $(ORACLE) $(REFLIB) $(DROPIN)
+
+.PHONY: all lib oracle ref cpptests clean

@@ -1,0 +1,189 @@
+/*
+ * fdgpu.h -- C ABI of the B200-native Richardson-Lucy hot path
+ *            (libfdgpu.so, hand-written sm_100a CUDA).
+ *
+ * The reference (fastdeconv, /root/reference/proj/include/fastdeconv) is a
+ * header-only C++20 library with no ABI of its own.  This header is the
+ * boundary its hot path is re-bound to: every entry point below replaces one
+ * reference function (cited per declaration), with plain pointers and sizes,
+ * int status codes instead of exceptions, and no torch / C++ types.  The C++
+ * drop-in headers (include/fastdeconv/{convolve,rl}.hpp) and the Python
+ * package (paper_1304_7211_b200) are thin marshalling layers over it.
+ *
+ * Images are row-major float32 planes, width*height (host entry points) or
+ * width x height with a row pitch in elements (device entry points; pitch a
+ * multiple of 4, pointers 16-byte aligned).  Arithmetic is fp32 on the device
+ * (the reference computes in fp64; the parity bound is max-rel <= 1e-4 after
+ * the configured iteration count).  There is no CPU fallback: without a CUDA
+ * device every compute entry point returns FDG_ECUDA.
+ */
+#ifndef FDGPU_H
+#define FDGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FDG_ABI_VERSION 1
+
+/* status codes: the reference's exception classes */
+#define FDG_OK 0
+#define FDG_EINVAL 1   /* std::invalid_argument (validation, dispatch)      */
+#define FDG_ENAN 2     /* std::runtime_error "NaN in iterate at iteration k" */
+#define FDG_ELOGIC 3   /* std::logic_error                                   */
+#define FDG_ECUDA 4    /* no device / CUDA failure (no fallback exists)      */
+
+/* OperatorKind, same numbering as convolve.hpp:22-32 */
+enum fdg_op {
+    FDG_OP_NAIVE = 0,
+    FDG_OP_LIST = 1,
+    FDG_OP_GENERIC_BOX = 2,
+    FDG_OP_BOX2D_SLIDING = 3,
+    FDG_OP_BOX2D_CUMUL = 4,
+    FDG_OP_BOX1D_SLIDING = 5,
+    FDG_OP_BOX1D_CUMUL = 6,
+    FDG_OP_FOURIER = 7,
+    FDG_OP_AUTO = 8
+};
+
+/* Psf variant alternative, psf.hpp:173 */
+enum fdg_repr { FDG_PSF_DENSE = 0, FDG_PSF_UNIFORM_CONVEX = 1, FDG_PSF_SPARSE = 2 };
+
+/* PSF as the reference stores it (normalised weights).
+ *   DensePsf          psf.hpp:26-70   width,height,anchor_x,anchor_y,weights[w*h]
+ *   UniformConvexPsf  psf.hpp:75-120  n_rows,row_dy[],row_xmin[],row_xmax[]
+ *   SparsePsf         psf.hpp:124-170 n_taps,tap_dx[],tap_dy[],tap_w[]          */
+typedef struct fdg_psf_desc {
+    int repr;
+    int width, height, anchor_x, anchor_y;
+    const double* weights;
+    int n_rows;
+    const int *row_dy, *row_xmin, *row_xmax;
+    int n_taps;
+    const int *tap_dx, *tap_dy;
+    const double* tap_w;
+} fdg_psf_desc;
+
+/* RlConfig, rl.hpp:18-23 */
+typedef struct fdg_rl_config {
+    int iterations;
+    int op;
+    double epsilon_div;
+    int clamp_nonnegative;
+} fdg_rl_config;
+
+/* RlIterationRecord, rl.hpp:25-30 */
+typedef struct fdg_rl_record {
+    int iteration;
+    double inactive_fraction;
+    double max_abs_change;
+    double seconds;
+} fdg_rl_record;
+
+typedef struct fdg_ctx fdg_ctx;
+typedef struct fdg_plan fdg_plan;
+typedef struct fdg_solver fdg_solver;
+
+int fdg_abi_version(void);
+/* last error message of this thread (ctx-independent) */
+const char* fdg_last_error(void);
+/* 1 when a CUDA device is usable, else 0 */
+int fdg_device_available(void);
+
+/* Context: device, stream (default: a private non-blocking stream). */
+int fdg_ctx_create(int device, fdg_ctx** out);
+void fdg_ctx_destroy(fdg_ctx* ctx);
+/* run on an external cudaStream_t (e.g. torch.cuda.current_stream()) */
+int fdg_ctx_set_stream(fdg_ctx* ctx, void* cuda_stream);
+int fdg_ctx_synchronize(fdg_ctx* ctx);
+/* number of kernel launches issued through this context so far */
+uint64_t fdg_ctx_launch_count(const fdg_ctx* ctx);
+
+/* ---- plan logic (host only; no device needed) ----------------------- */
+/* dispatch(), convolve.hpp:627-643 -> *kind, or FDG_EINVAL naming op+PSF */
+int fdg_dispatch(const fdg_psf_desc* psf, int preference, int* kind);
+/* operatorAcceptsPsf(), convolve.hpp:607-625 */
+int fdg_operator_accepts(int kind, const fdg_psf_desc* psf, int* accepts);
+
+/* ConvPlan(psf, preference), convolve.hpp:652-676 */
+int fdg_plan_create(fdg_ctx* ctx, const fdg_psf_desc* psf, int preference, fdg_plan** out);
+void fdg_plan_destroy(fdg_plan* plan);
+/* ConvPlan::kind(), convolve.hpp:678 */
+int fdg_plan_kind(const fdg_plan* plan);
+/* ConvCounters the reference operator would report for one width x height
+ * application (convolve.hpp:140-143,165-167,206-210,239-243,274-278,
+ * 315-318,328,339-341,372,383-386); analytic, no device work. */
+int fdg_plan_counters(const fdg_plan* plan, int width, int height, uint64_t counters[3]);
+/* the same counters without a device: dispatch + analytic formulas */
+int fdg_op_counters(const fdg_psf_desc* psf, int preference, int width, int height,
+                    uint64_t counters[3]);
+/* which device engine serves the plan: "rows", "box2d", "spans", "dense",
+ * "taps" or "cyclic" (diagnostics / bench labels) */
+const char* fdg_plan_engine(const fdg_plan* plan);
+
+/* ConvPlan::applyInto, convolve.hpp:680-715 (host buffers) */
+int fdg_conv_apply(fdg_plan* plan, const float* in, int width, int height, float* out);
+/* ConvPlan::applyMaskedInto, convolve.hpp:724-736: only Naive and List plans,
+ * else FDG_EINVAL "operator does not support masked evaluation" */
+int fdg_conv_apply_masked(fdg_plan* plan, const float* in, int width, int height,
+                          const uint8_t* active, const float* fallback, float* out);
+/* device-resident variant on the context stream */
+int fdg_conv_apply_device(fdg_plan* plan, const float* d_in, float* d_out, int width, int height,
+                          int pitch);
+
+/* ---- Richardson-Lucy drivers (host buffers) ------------------------- */
+/* rlDeconvolve, rl.hpp:140-179.  trace: nullable, cfg->iterations records */
+int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg,
+                      const float* f, int width, int height, float* u_out, fdg_rl_record* trace);
+/* rlDeconvolveSelective, rl.hpp:187-257.  thin_start: deactivation is held
+ * off for 0-based k < thin_start (0 = the reference).  mask_replay
+ * (nullable, iterations*width*height bytes) replaces the device's own
+ * deactivation decisions with recorded masks; mask_record (nullable) gets
+ * the mask each iteration's convolutions used. */
+int fdg_rl_deconvolve_selective(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg,
+                                double threshold, int period, int thin_start,
+                                const uint8_t* mask_replay, uint8_t* mask_record, const float* f,
+                                int width, int height, float* u_out, fdg_rl_record* trace);
+/* rlStep, rl.hpp:131-137 */
+int fdg_rl_step(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg, const float* u,
+                const float* f, int width, int height, float* u_out, double* max_abs_change);
+
+/* ---- device-resident solver (bench, sharding, batches) --------------- */
+/* Plans for h and adjoint(h) + per-iteration trace arrays, for `batch`
+ * images of width x height (rows of a shard may carry halos: see
+ * fdg_solver_pass). */
+int fdg_solver_create(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg, int width,
+                      int height, int batch, fdg_solver** out);
+void fdg_solver_destroy(fdg_solver* s);
+/* Full RL loop in place on device buffers: u <- f, then cfg->iterations
+ * iterations (q is a solver-owned scratch plane).  Images are `batch`
+ * planes of height rows each, `image_stride` elements apart. */
+int fdg_solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long image_stride,
+                   int iterations);
+/* One fused pass over output rows [y0, y1) of each image, reading input rows
+ * clamped to [ylo, yhi] (relative to the same row 0; halos of a row strip
+ * are rows < 0 or >= height).  pass 1: out = aux / max(h (x) in, eps)
+ * (aux = f);  pass 2: out = max(h* (x) in * aux, 0) (aux = u; out may alias
+ * aux) with max|du| and NaN accumulated into trace slot `iteration`. */
+int fdg_solver_pass(fdg_solver* s, int pass, const float* d_in, const float* d_aux, float* d_out,
+                    int pitch, long long image_stride, int y0, int y1, int ylo, int yhi,
+                    int iteration);
+/* copy per-iteration {max|du|, NaN} back (synchronises) */
+int fdg_solver_trace(fdg_solver* s, fdg_rl_record* out, int n);
+int fdg_solver_reset_trace(fdg_solver* s);
+
+/* ---- stream compaction (selective path) ------------------------------ */
+/* Row-major active list and (y, x0, len) runs of a device mask, the order
+ * of the reference's run walk (convolve.hpp:450-465).  Host buffers out;
+ * returns counts through n_active / n_runs (buffers may be NULL to query). */
+int fdg_mask_compact(fdg_ctx* ctx, const uint8_t* active, int width, int height,
+                     int64_t* idx, int64_t idx_cap, int64_t* n_active, int32_t* runs,
+                     int64_t runs_cap, int64_t* n_runs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

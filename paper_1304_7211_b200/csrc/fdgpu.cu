@@ -1,0 +1,1016 @@
+// fdgpu.cu -- the C ABI (include/fdgpu.h): contexts, plans, one-shot
+// operators, the HBM-resident Richardson-Lucy drivers and the device solver.
+//
+// RL iteration on the device (rl.hpp:153-177 restated as two fused passes):
+//   pass 1  q  = f / max(h (x) u, eps)          conv + quotient epilogue
+//   pass 2  u' = max(h* (x) q * u, 0)           conv + update epilogue,
+//             max|u'-u| and a NaN flag reduced into per-iteration slots
+// u, f and q stay resident in HBM for the whole run; u is updated in place
+// (pass 2 reads u only at the output pixel).  24 B/px.it of algorithmic
+// traffic: pass 1 reads u, f and writes q; pass 2 reads q, u and writes u.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace fdg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_err(cudaError_t e, const char* where) {
+    return set_err(FDG_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                              \
+    do {                                                      \
+        cudaError_t _e = (call);                              \
+        if (_e != cudaSuccess) return cuda_err(_e, #call);    \
+    } while (0)
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    cudaError_t ensure(size_t count) {
+        if (count <= n) return cudaSuccess;
+        release();
+        cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+        if (e == cudaSuccess) n = count;
+        return e;
+    }
+};
+
+int pitch_for(int W) { return (W + 31) & ~31; }  // 128-byte rows
+
+}  // namespace
+
+struct fdg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint64_t launches = 0;
+    // scratch for the host-buffer entry points
+    DevBuf<float> a, b, c, d;
+    DevBuf<uint8_t> m;
+};
+
+struct fdg_plan {
+    fdg_ctx* ctx = nullptr;
+    int kind = FDG_OP_NAIVE;
+    HostPsf psf;  // the representation the plan stores (ConvPlan members)
+    LineShape line{};
+    RectShape rect{};
+    std::vector<Span> spans;
+    std::vector<Tap> taps;  // list / naive tap view
+    DevPsf dev;
+    int wrap = 0;
+    // masked dense path: compacted per-tile block lists
+    DevBuf<int> tile_blocks, tile_count;
+    ~fdg_plan() {
+        cudaFree(dev.d_row_start);
+        cudaFree(dev.d_dx);
+        cudaFree(dev.d_w);
+        cudaFree(dev.d_span);
+        cudaFree(dev.d_dense);
+    }
+};
+
+struct fdg_solver {
+    fdg_ctx* ctx = nullptr;
+    std::unique_ptr<fdg_plan> fwd, adj;
+    fdg_rl_config cfg{};
+    int W = 0, H = 0, batch = 1;
+    int ntrace = 0;
+    DevBuf<float> q;
+    DevBuf<unsigned> maxchange;
+    DevBuf<int> nanflag;
+};
+
+namespace {
+
+const char* engine_name(int e) {
+    switch (e) {
+        case ENG_RECT: return "box";
+        case ENG_SPANS: return "spans";
+        case ENG_DENSE: return "dense";
+        case ENG_TAPS: return "taps";
+        case ENG_CYCLIC: return "cyclic";
+    }
+    return "?";
+}
+
+template <typename T>
+cudaError_t upload(T** dst, const std::vector<T>& v) {
+    cudaError_t e = cudaMalloc(dst, std::max<size_t>(v.size(), 1) * sizeof(T));
+    if (e != cudaSuccess) return e;
+    if (!v.empty()) e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+}
+
+// Taps grouped by PSF row (rows r = dy - min_dy, stable within a row).
+int build_taps_engine(fdg_plan* pl, const std::vector<Tap>& taps, bool uniform, double uniform_w) {
+    DevPsf& d = pl->dev;
+    d.engine = pl->wrap ? ENG_CYCLIC : ENG_TAPS;
+    d.min_dx = d.max_dx = taps[0].dx;
+    d.min_dy = d.max_dy = taps[0].dy;
+    for (const Tap& t : taps) {
+        d.min_dx = std::min(d.min_dx, t.dx);
+        d.max_dx = std::max(d.max_dx, t.dx);
+        d.min_dy = std::min(d.min_dy, t.dy);
+        d.max_dy = std::max(d.max_dy, t.dy);
+    }
+    d.nrows = d.max_dy - d.min_dy + 1;
+    d.ntaps = (int)taps.size();
+    std::vector<int> start(d.nrows + 1, 0), dx;
+    std::vector<float> w;
+    std::vector<std::vector<const Tap*>> rows(d.nrows);
+    for (const Tap& t : taps) rows[t.dy - d.min_dy].push_back(&t);
+    for (int r = 0; r < d.nrows; ++r) {
+        start[r] = (int)dx.size();
+        for (const Tap* t : rows[r]) {
+            dx.push_back(t->dx);
+            w.push_back((float)t->w);
+        }
+    }
+    start[d.nrows] = (int)dx.size();
+    d.uniform = uniform ? 1 : 0;
+    d.scale = uniform ? (float)uniform_w : 1.f;
+    CK(upload(&d.d_row_start, start));
+    CK(upload(&d.d_dx, dx));
+    CK(upload(&d.d_w, w));
+    return FDG_OK;
+}
+
+int build_plan(fdg_ctx* ctx, const HostPsf& psf, int preference, std::unique_ptr<fdg_plan>* out) {
+    std::string err;
+    const int kind = psf_dispatch(psf, preference, &err);
+    if (kind < 0) return set_err(FDG_EINVAL, err);
+    auto pl = std::make_unique<fdg_plan>();
+    pl->ctx = ctx;
+    pl->kind = kind;
+    pl->psf = psf;
+    DevPsf& d = pl->dev;
+    switch (kind) {
+        case FDG_OP_BOX1D_SLIDING:
+        case FDG_OP_BOX1D_CUMUL:
+        case FDG_OP_BOX2D_SLIDING:
+        case FDG_OP_BOX2D_CUMUL: {
+            if (kind == FDG_OP_BOX1D_SLIDING || kind == FDG_OP_BOX1D_CUMUL) {
+                psf_as_line(psf, &pl->line);
+                pl->rect = {pl->line.length, 1, pl->line.min_dx, pl->line.dy};
+            } else {
+                psf_as_rect(psf, &pl->rect);
+            }
+            const RectShape& r = pl->rect;
+            // scale as the reference multiplies it: 1/length resp. 1/(mx*my) in double
+            const double scale = (kind == FDG_OP_BOX1D_SLIDING || kind == FDG_OP_BOX1D_CUMUL)
+                                     ? 1.0 / (double)r.mx
+                                     : 1.0 / ((double)r.mx * (double)r.my);
+            if (rect_supported(r.mx)) {
+                d.engine = ENG_RECT;
+                d.mx = r.mx;
+                d.my = r.my;
+                d.min_dx = r.min_dx;
+                d.max_dx = r.min_dx + r.mx - 1;
+                d.min_dy = r.min_dy;
+                d.max_dy = r.min_dy + r.my - 1;
+                d.uniform = 1;
+                d.scale = (float)scale;
+            } else {
+                std::vector<Tap> t;
+                for (int y = 0; y < r.my; ++y)
+                    for (int x = 0; x < r.mx; ++x) t.push_back({r.min_dx + x, r.min_dy + y, scale});
+                int st = build_taps_engine(pl.get(), t, true, scale);
+                if (st) return st;
+            }
+            break;
+        }
+        case FDG_OP_GENERIC_BOX: {
+            psf_as_convex(psf, &pl->spans);
+            int count = 0;
+            std::vector<Tap> t;
+            for (const Span& s : pl->spans) count += s.xmax - s.xmin + 1;
+            const double u = 1.0 / (double)count;
+            for (const Span& s : pl->spans)
+                for (int x = s.xmin; x <= s.xmax; ++x) t.push_back({x, s.dy, u});
+            int st = build_taps_engine(pl.get(), t, true, u);
+            if (st) return st;
+            break;
+        }
+        case FDG_OP_LIST: {
+            pl->taps = psf_taps(psf);
+            int st = build_taps_engine(pl.get(), pl->taps, false, 1.0);
+            if (st) return st;
+            break;
+        }
+        case FDG_OP_NAIVE:
+        case FDG_OP_FOURIER: {
+            // toDense (psf.hpp:336-375): the grid keeps the origin inside it
+            HostPsf dense = psf;
+            if (psf.repr != FDG_PSF_DENSE) {
+                const std::vector<Tap> t = psf_taps(psf);
+                int x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+                for (const Tap& q : t) {
+                    x0 = std::min(x0, q.dx);
+                    x1 = std::max(x1, q.dx);
+                    y0 = std::min(y0, q.dy);
+                    y1 = std::max(y1, q.dy);
+                }
+                dense = HostPsf{};
+                dense.repr = FDG_PSF_DENSE;
+                dense.w = x1 - x0 + 1;
+                dense.h = y1 - y0 + 1;
+                dense.ax = -x0;
+                dense.ay = -y0;
+                dense.weights.assign((size_t)dense.w * dense.h, 0.0);
+                for (const Tap& q : t) dense.weights[(size_t)(q.dy - y0) * dense.w + (q.dx - x0)] += q.w;
+            }
+            pl->psf = dense;
+            pl->wrap = kind == FDG_OP_FOURIER;
+            d.mw = dense.w;
+            d.mh = dense.h;
+            if (kind == FDG_OP_NAIVE && dense_supported(d)) {
+                d.engine = ENG_DENSE;
+                d.mwp = d.mw <= 4 ? 4 : d.mw <= 8 ? 8 : d.mw <= 16 ? 16 : 32;
+                d.min_dx = -dense.ax;
+                d.max_dx = d.min_dx + d.mwp - 1;  // padded columns carry zero weight
+                d.min_dy = -dense.ay;
+                d.max_dy = d.min_dy + d.mh - 1;
+                std::vector<float> w((size_t)d.mh * d.mwp, 0.f);
+                for (int y = 0; y < d.mh; ++y)
+                    for (int x = 0; x < d.mw; ++x) w[(size_t)y * d.mwp + x] = (float)dense.weights[(size_t)y * d.mw + x];
+                CK(upload(&d.d_dense, w));
+            } else {
+                std::vector<Tap> t;
+                for (int y = 0; y < dense.h; ++y)
+                    for (int x = 0; x < dense.w; ++x) {
+                        const double w = dense.weights[(size_t)y * dense.w + x];
+                        if (w != 0.0) t.push_back({x - dense.ax, y - dense.ay, w});
+                    }
+                int st = build_taps_engine(pl.get(), t, false, 1.0);
+                if (st) return st;
+            }
+            break;
+        }
+        default:
+            return set_err(FDG_ELOGIC, "ConvPlan: unresolved operator");
+    }
+    *out = std::move(pl);
+    return FDG_OK;
+}
+
+// One fused pass of `pl` over geometry g with epilogue e.
+int run_pass(fdg_plan* pl, const Geom& g, const Epi& e, cudaStream_t st) {
+    cudaError_t r = cudaSuccess;
+    const DevPsf& d = pl->dev;
+    const bool masked = e.active != nullptr;
+    switch (d.engine) {
+        case ENG_RECT:
+            if (masked) return set_err(FDG_EINVAL, "operator does not support masked evaluation");
+            r = launch_rect(d, g, e, st);
+            break;
+        case ENG_SPANS:
+            if (masked) return set_err(FDG_EINVAL, "operator does not support masked evaluation");
+            r = launch_spans(d, g, e, st);
+            break;
+        case ENG_DENSE:
+            if (masked) {
+                const DenseTiling t = dense_tiling(g.W, g.y1 - g.y0);
+                const size_t tiles = (size_t)t.tiles_x * t.tiles_y;
+                if ((r = pl->tile_blocks.ensure(tiles * 256)) != cudaSuccess) break;
+                if ((r = pl->tile_count.ensure(tiles)) != cudaSuccess) break;
+                if (g.batch != 1 || g.y0 != 0) return set_err(FDG_EINVAL, "masked dense pass: single image only");
+                r = launch_tile_compact(e.active, g.W, g.y1, g.pitch, pl->tile_blocks.p, pl->tile_count.p,
+                                        nullptr, st);
+                if (r == cudaSuccess) r = launch_dense(d, g, e, st, pl->tile_blocks.p, pl->tile_count.p);
+                pl->ctx->launches += 1;
+            } else {
+                r = launch_dense(d, g, e, st, nullptr, nullptr);
+            }
+            break;
+        case ENG_TAPS:
+        case ENG_CYCLIC: {
+            Geom gg = g;
+            gg.wrap = d.engine == ENG_CYCLIC;
+            r = launch_taps(d, gg, e, st);
+            break;
+        }
+    }
+    if (r != cudaSuccess) return cuda_err(r, "kernel launch");
+    pl->ctx->launches += 1;
+    return FDG_OK;
+}
+
+Geom whole(const float* in, float* out, int pitch, int W, int H, int batch = 1, long long bstride = 0) {
+    Geom g;
+    g.in = in;
+    g.out = out;
+    g.pitch = pitch;
+    g.W = W;
+    g.y0 = 0;
+    g.y1 = H;
+    g.ylo = 0;
+    g.yhi = H - 1;
+    g.batch = batch;
+    g.bstride = bstride;
+    return g;
+}
+
+int check_device(fdg_ctx* ctx) {
+    if (!ctx) return set_err(FDG_ECUDA, "no CUDA context (no device available; the B200 path has no CPU fallback)");
+    CK(cudaSetDevice(ctx->device));
+    return FDG_OK;
+}
+
+int h2d(float* d, int pitch, const float* h, int W, int H, cudaStream_t st) {
+    CK(cudaMemcpy2DAsync(d, (size_t)pitch * 4, h, (size_t)W * 4, (size_t)W * 4, H, cudaMemcpyHostToDevice, st));
+    return FDG_OK;
+}
+int d2h(float* h, const float* d, int pitch, int W, int H, cudaStream_t st) {
+    CK(cudaMemcpy2DAsync(h, (size_t)W * 4, d, (size_t)pitch * 4, (size_t)W * 4, H, cudaMemcpyDeviceToHost, st));
+    return FDG_OK;
+}
+
+int validate_rl(const float* f, int W, int H, const fdg_rl_config* cfg, const char* where) {
+    const std::string w(where);
+    if (!f || W < 1 || H < 1) return set_err(FDG_EINVAL, w + ": empty input image");
+    if (!cfg) return set_err(FDG_EINVAL, w + ": null config");
+    if (cfg->iterations < 0) return set_err(FDG_EINVAL, w + ": iterations must be >= 0");
+    if (!(cfg->epsilon_div > 0.0)) return set_err(FDG_EINVAL, w + ": epsilonDiv must be positive");
+    const size_t n = (size_t)W * H;
+    for (size_t i = 0; i < n; ++i) {
+        if (!std::isfinite(f[i])) return set_err(FDG_EINVAL, w + ": input image has non-finite pixels");
+        if (f[i] < 0.f) return set_err(FDG_EINVAL, w + ": input image must be nonnegative");
+    }
+    return FDG_OK;
+}
+
+int make_rl_plans(fdg_ctx* ctx, const fdg_psf_desc* desc, int op, std::unique_ptr<fdg_plan>* fwd,
+                  std::unique_ptr<fdg_plan>* adj, int force_kind = -1) {
+    HostPsf h;
+    std::string err;
+    if (!psf_from_desc(desc, &h, &err)) return set_err(FDG_EINVAL, err);
+    int st = build_plan(ctx, h, force_kind >= 0 ? force_kind : op, fwd);
+    if (st) return st;
+    // ConvPlan(adjoint(h), forward.kind()), rl.hpp:143
+    return build_plan(ctx, psf_adjoint(h), (*fwd)->kind, adj);
+}
+
+struct EventPool {
+    std::vector<cudaEvent_t> ev;
+    ~EventPool() {
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
+    cudaError_t make(int n) {
+        ev.resize(n, nullptr);
+        for (int i = 0; i < n; ++i) {
+            cudaError_t e = cudaEventCreate(&ev[i]);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
+};
+
+}  // namespace
+
+// =========================================================== ABI functions
+extern "C" {
+
+int fdg_abi_version(void) { return FDG_ABI_VERSION; }
+const char* fdg_last_error(void) { return g_err.c_str(); }
+
+int fdg_device_available(void) {
+    int n = 0;
+    return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+}
+
+int fdg_ctx_create(int device, fdg_ctx** out) {
+    if (!out) return set_err(FDG_EINVAL, "null output");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return set_err(FDG_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    if (device < 0 || device >= n) return set_err(FDG_EINVAL, "device index out of range");
+    CK(cudaSetDevice(device));
+    auto* c = new fdg_ctx();
+    c->device = device;
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_err(e, "cudaStreamCreate");
+    }
+    c->own_stream = true;
+    *out = c;
+    return FDG_OK;
+}
+
+void fdg_ctx_destroy(fdg_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int fdg_ctx_set_stream(fdg_ctx* ctx, void* stream) {
+    if (!ctx) return set_err(FDG_EINVAL, "null context");
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    ctx->stream = (cudaStream_t)stream;
+    ctx->own_stream = false;
+    return FDG_OK;
+}
+
+int fdg_ctx_synchronize(fdg_ctx* ctx) {
+    if (!ctx) return set_err(FDG_EINVAL, "null context");
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FDG_OK;
+}
+
+uint64_t fdg_ctx_launch_count(const fdg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int fdg_dispatch(const fdg_psf_desc* desc, int preference, int* kind) {
+    HostPsf h;
+    std::string err;
+    if (!psf_from_desc(desc, &h, &err)) return set_err(FDG_EINVAL, err);
+    const int k = psf_dispatch(h, preference, &err);
+    if (k < 0) return set_err(FDG_EINVAL, err);
+    if (kind) *kind = k;
+    return FDG_OK;
+}
+
+int fdg_operator_accepts(int kind, const fdg_psf_desc* desc, int* accepts) {
+    HostPsf h;
+    std::string err;
+    if (!psf_from_desc(desc, &h, &err)) return set_err(FDG_EINVAL, err);
+    if (accepts) *accepts = psf_accepts(kind, h) ? 1 : 0;
+    return FDG_OK;
+}
+
+int fdg_plan_create(fdg_ctx* ctx, const fdg_psf_desc* desc, int preference, fdg_plan** out) {
+    int st = check_device(ctx);
+    if (st) return st;
+    HostPsf h;
+    std::string err;
+    if (!psf_from_desc(desc, &h, &err)) return set_err(FDG_EINVAL, err);
+    std::unique_ptr<fdg_plan> pl;
+    st = build_plan(ctx, h, preference, &pl);
+    if (st) return st;
+    *out = pl.release();
+    return FDG_OK;
+}
+
+void fdg_plan_destroy(fdg_plan* plan) { delete plan; }
+int fdg_plan_kind(const fdg_plan* plan) { return plan ? plan->kind : -1; }
+const char* fdg_plan_engine(const fdg_plan* plan) { return plan ? engine_name(plan->dev.engine) : "?"; }
+
+}  // extern "C"
+
+namespace {
+// ConvCounters of one W x H application of the operator `kind` on `psf`
+void counters_for(int kind, const HostPsf& psf, int W, int H, uint64_t c[3]) {
+    const uint64_t nx = (uint64_t)W, ny = (uint64_t)H;
+    c[0] = c[1] = c[2] = 0;
+    switch (kind) {
+        case FDG_OP_NAIVE: {  // convolve.hpp:140-143 (toDense grid, origin included)
+            int w = psf.w, h = psf.h;
+            if (psf.repr != FDG_PSF_DENSE) {
+                int x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+                for (const Tap& t : psf_taps(psf)) {
+                    x0 = std::min(x0, t.dx);
+                    x1 = std::max(x1, t.dx);
+                    y0 = std::min(y0, t.dy);
+                    y1 = std::max(y1, t.dy);
+                }
+                w = x1 - x0 + 1;
+                h = y1 - y0 + 1;
+            }
+            c[0] = nx * ny;
+            c[1] = nx * ny * (uint64_t)w * h;
+            break;
+        }
+        case FDG_OP_LIST:  // :165-167
+            c[0] = nx * ny;
+            c[1] = nx * ny * (uint64_t)psf_taps(psf).size();
+            break;
+        case FDG_OP_GENERIC_BOX: {  // :206-210
+            std::vector<Span> spans;
+            psf_as_convex(psf, &spans);
+            uint64_t support = 0;
+            for (const Span& s : spans) support += s.xmax - s.xmin + 1;
+            c[0] = nx * ny;
+            c[2] = support * ny;
+            c[1] = (nx - 1) * 2 * (uint64_t)spans.size() * ny;
+            break;
+        }
+        case FDG_OP_BOX1D_SLIDING: {  // :239-243
+            LineShape l{};
+            psf_as_line(psf, &l);
+            c[0] = nx * ny;
+            c[2] = (uint64_t)l.length * ny;
+            c[1] = (nx - 1) * 2 * ny;
+            break;
+        }
+        case FDG_OP_BOX1D_CUMUL: {  // :274-278
+            LineShape ln{};
+            psf_as_line(psf, &ln);
+            const int l = std::max(0, -ln.min_dx), r = std::max(0, ln.min_dx + ln.length - 1);
+            c[0] = nx * ny;
+            c[2] = (uint64_t)(W + l + r) * ny;
+            c[1] = nx * 2 * ny;
+            break;
+        }
+        case FDG_OP_BOX2D_SLIDING: {  // :315-318, 328, 339-341
+            RectShape r{};
+            psf_as_rect(psf, &r);
+            const int t = std::max(0, -r.min_dy), b = std::max(0, r.min_dy + r.my - 1);
+            const uint64_t ph = ny + t + b;
+            c[2] = ph * (uint64_t)r.mx + nx * (uint64_t)r.my;
+            c[1] = ph * (nx - 1) * 2 + (ny - 1) * nx * 2;
+            c[0] = nx * ny;
+            break;
+        }
+        case FDG_OP_BOX2D_CUMUL: {  // :372, 383-386
+            RectShape r{};
+            psf_as_rect(psf, &r);
+            const int l = std::max(0, -r.min_dx), rr = std::max(0, r.min_dx + r.mx - 1);
+            const int t = std::max(0, -r.min_dy), b = std::max(0, r.min_dy + r.my - 1);
+            c[2] = (uint64_t)(W + l + rr) * (uint64_t)(H + t + b) * 3;
+            c[0] = nx * ny;
+            c[1] = nx * ny * 4;
+            break;
+        }
+        default:
+            break;  // Fourier reports nothing (convolve.hpp:394-418)
+    }
+}
+}  // namespace
+
+extern "C" {
+int fdg_plan_counters(const fdg_plan* pl, int W, int H, uint64_t c[3]) {
+    if (!pl || !c) return set_err(FDG_EINVAL, "null argument");
+    counters_for(pl->kind, pl->psf, W, H, c);
+    return FDG_OK;
+}
+
+int fdg_op_counters(const fdg_psf_desc* desc, int preference, int W, int H, uint64_t c[3]) {
+    HostPsf h;
+    std::string err;
+    if (!c) return set_err(FDG_EINVAL, "null argument");
+    if (!psf_from_desc(desc, &h, &err)) return set_err(FDG_EINVAL, err);
+    const int kind = psf_dispatch(h, preference, &err);
+    if (kind < 0) return set_err(FDG_EINVAL, err);
+    counters_for(kind, h, W, H, c);
+    return FDG_OK;
+}
+}  // extern "C"
+
+extern "C" {
+int fdg_conv_apply(fdg_plan* pl, const float* in, int W, int H, float* out) {
+    if (!pl || !in || !out) return set_err(FDG_EINVAL, "null argument");
+    if (W < 1 || H < 1) return set_err(FDG_EINVAL, "Image: dimensions must be at least 1x1");
+    fdg_ctx* ctx = pl->ctx;
+    int st = check_device(ctx);
+    if (st) return st;
+    const int pitch = pitch_for(W);
+    const size_t n = (size_t)pitch * H;
+    CK(ctx->a.ensure(n));
+    CK(ctx->b.ensure(n));
+    if ((st = h2d(ctx->a.p, pitch, in, W, H, ctx->stream))) return st;
+    Epi e;
+    e.mode = EPI_STORE;
+    if ((st = run_pass(pl, whole(ctx->a.p, ctx->b.p, pitch, W, H), e, ctx->stream))) return st;
+    if ((st = d2h(out, ctx->b.p, pitch, W, H, ctx->stream))) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FDG_OK;
+}
+
+int fdg_conv_apply_device(fdg_plan* pl, const float* d_in, float* d_out, int W, int H, int pitch) {
+    if (!pl || !d_in || !d_out) return set_err(FDG_EINVAL, "null argument");
+    if (pitch % 4 || pitch < W) return set_err(FDG_EINVAL, "pitch must be a multiple of 4 and >= width");
+    Epi e;
+    e.mode = EPI_STORE;
+    return run_pass(pl, whole(d_in, d_out, pitch, W, H), e, pl->ctx->stream);
+}
+
+int fdg_conv_apply_masked(fdg_plan* pl, const float* in, int W, int H, const uint8_t* active,
+                          const float* fallback, float* out) {
+    if (!pl || !in || !out || !active || !fallback) return set_err(FDG_EINVAL, "null argument");
+    if (pl->kind != FDG_OP_NAIVE && pl->kind != FDG_OP_LIST)
+        return set_err(FDG_EINVAL, "operator does not support masked evaluation");
+    fdg_ctx* ctx = pl->ctx;
+    int st = check_device(ctx);
+    if (st) return st;
+    const int pitch = pitch_for(W);
+    const size_t n = (size_t)pitch * H;
+    CK(ctx->a.ensure(n));
+    CK(ctx->b.ensure(n));
+    CK(ctx->m.ensure(n));
+    if ((st = h2d(ctx->a.p, pitch, in, W, H, ctx->stream))) return st;
+    if ((st = h2d(ctx->b.p, pitch, fallback, W, H, ctx->stream))) return st;
+    CK(launch_fill_u8(ctx->m.p, 1, n, ctx->stream));
+    CK(cudaMemcpy2DAsync(ctx->m.p, pitch, active, W, W, H, cudaMemcpyHostToDevice, ctx->stream));
+    Epi e;
+    e.mode = EPI_STORE;
+    e.active = ctx->m.p;
+    if ((st = run_pass(pl, whole(ctx->a.p, ctx->b.p, pitch, W, H), e, ctx->stream))) return st;
+    if ((st = d2h(out, ctx->b.p, pitch, W, H, ctx->stream))) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FDG_OK;
+}
+
+int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, const float* f, int W,
+                      int H, float* u_out, fdg_rl_record* trace) {
+    int st = validate_rl(f, W, H, cfg, "rlDeconvolve");
+    if (st) return st;
+    if ((st = check_device(ctx))) return st;
+    std::unique_ptr<fdg_plan> fwd, adj;
+    if ((st = make_rl_plans(ctx, desc, cfg->op, &fwd, &adj))) return st;
+    const int iters = cfg->iterations;
+    const int pitch = pitch_for(W);
+    const size_t n = (size_t)pitch * H;
+    cudaStream_t s = ctx->stream;
+    DevBuf<float> df, du, dq;
+    DevBuf<unsigned> mc;
+    DevBuf<int> nf;
+    CK(df.ensure(n));
+    CK(du.ensure(n));
+    CK(dq.ensure(n));
+    CK(mc.ensure(iters + 1));
+    CK(nf.ensure(iters + 1));
+    CK(cudaMemsetAsync(mc.p, 0, sizeof(unsigned) * (iters + 1), s));
+    CK(cudaMemsetAsync(nf.p, 0, sizeof(int) * (iters + 1), s));
+    if ((st = h2d(df.p, pitch, f, W, H, s))) return st;
+    CK(cudaMemcpyAsync(du.p, df.p, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    EventPool ev;
+    CK(ev.make(iters + 1));
+    CK(cudaEventRecord(ev.ev[0], s));
+    for (int k = 0; k < iters; ++k) {
+        Epi e1;
+        e1.mode = EPI_QUOT;
+        e1.aux = df.p;
+        e1.eps = (float)cfg->epsilon_div;
+        if ((st = run_pass(fwd.get(), whole(du.p, dq.p, pitch, W, H), e1, s))) return st;
+        Epi e2;
+        e2.mode = EPI_UPDATE;
+        e2.aux = du.p;
+        e2.clamp = cfg->clamp_nonnegative;
+        e2.maxchange = mc.p + k;
+        e2.nanflag = nf.p + k;
+        if ((st = run_pass(adj.get(), whole(dq.p, du.p, pitch, W, H), e2, s))) return st;
+        CK(cudaEventRecord(ev.ev[k + 1], s));
+    }
+    if ((st = d2h(u_out, du.p, pitch, W, H, s))) return st;
+    std::vector<unsigned> hmc(iters + 1);
+    std::vector<int> hnf(iters + 1);
+    CK(cudaMemcpyAsync(hmc.data(), mc.p, sizeof(unsigned) * (iters + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hnf.data(), nf.p, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < iters; ++k) {
+        if (hnf[k])
+            return set_err(FDG_ENAN, "rlDeconvolve: NaN in iterate at iteration " + std::to_string(k + 1));
+        if (trace) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev.ev[k], ev.ev[k + 1]);
+            float m;
+            std::memcpy(&m, &hmc[k], sizeof m);
+            trace[k] = {k + 1, 0.0, (double)m, ms * 1e-3};
+        }
+    }
+    return FDG_OK;
+}
+
+int fdg_rl_step(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, const float* u, const float* f,
+                int W, int H, float* u_out, double* max_abs_change) {
+    if (!u || !f || !u_out || !cfg) return set_err(FDG_EINVAL, "null argument");
+    if (W < 1 || H < 1) return set_err(FDG_EINVAL, "rlStep: image dimensions differ");
+    int st = check_device(ctx);
+    if (st) return st;
+    std::unique_ptr<fdg_plan> fwd, adj;
+    if ((st = make_rl_plans(ctx, desc, cfg->op, &fwd, &adj))) return st;
+    const int pitch = pitch_for(W);
+    const size_t n = (size_t)pitch * H;
+    cudaStream_t s = ctx->stream;
+    DevBuf<float> df, du, dq;
+    DevBuf<unsigned> mc;
+    DevBuf<int> nf;
+    CK(df.ensure(n));
+    CK(du.ensure(n));
+    CK(dq.ensure(n));
+    CK(mc.ensure(1));
+    CK(nf.ensure(1));
+    CK(cudaMemsetAsync(mc.p, 0, sizeof(unsigned), s));
+    CK(cudaMemsetAsync(nf.p, 0, sizeof(int), s));
+    if ((st = h2d(df.p, pitch, f, W, H, s))) return st;
+    if ((st = h2d(du.p, pitch, u, W, H, s))) return st;
+    Epi e1;
+    e1.mode = EPI_QUOT;
+    e1.aux = df.p;
+    e1.eps = (float)cfg->epsilon_div;
+    if ((st = run_pass(fwd.get(), whole(du.p, dq.p, pitch, W, H), e1, s))) return st;
+    Epi e2;
+    e2.mode = EPI_UPDATE;
+    e2.aux = du.p;
+    e2.clamp = cfg->clamp_nonnegative;
+    e2.maxchange = mc.p;
+    e2.nanflag = nf.p;
+    if ((st = run_pass(adj.get(), whole(dq.p, du.p, pitch, W, H), e2, s))) return st;
+    if ((st = d2h(u_out, du.p, pitch, W, H, s))) return st;
+    unsigned m = 0;
+    CK(cudaMemcpyAsync(&m, mc.p, sizeof m, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (max_abs_change) {
+        float fm;
+        std::memcpy(&fm, &m, sizeof fm);
+        *max_abs_change = fm;
+    }
+    return FDG_OK;
+}
+
+int fdg_rl_deconvolve_selective(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, double threshold,
+                                int period, int thin_start, const uint8_t* mask_replay, uint8_t* mask_record,
+                                const float* f, int W, int H, float* u_out, fdg_rl_record* trace) {
+    int st = validate_rl(f, W, H, cfg, "rlDeconvolveSelective");
+    if (st) return st;
+    if (threshold < 0.0) return set_err(FDG_EINVAL, "rlDeconvolveSelective: threshold must be >= 0");
+    if (period < 1) return set_err(FDG_EINVAL, "rlDeconvolveSelective: reactivation period must be >= 1");
+    // rl.hpp:195-199: Auto -> List for SparsePsf else Naive; others refuse
+    int kind = cfg->op;
+    if (kind == FDG_OP_AUTO) kind = desc && desc->repr == FDG_PSF_SPARSE ? FDG_OP_LIST : FDG_OP_NAIVE;
+    if (kind != FDG_OP_NAIVE && kind != FDG_OP_LIST)
+        return set_err(FDG_EINVAL, "operator does not support masked evaluation");
+    if ((st = check_device(ctx))) return st;
+    std::unique_ptr<fdg_plan> fwd, adj;
+    if ((st = make_rl_plans(ctx, desc, kind, &fwd, &adj))) return st;
+    const int iters = cfg->iterations;
+    const int pitch = pitch_for(W);
+    const size_t n = (size_t)pitch * H;
+    cudaStream_t s = ctx->stream;
+    DevBuf<float> df, du, dq, dv;
+    DevBuf<uint8_t> dm;
+    DevBuf<unsigned> mc;
+    DevBuf<int> nf;
+    DevBuf<unsigned long long> ni;
+    CK(df.ensure(n));
+    CK(du.ensure(n));
+    CK(dq.ensure(n));
+    CK(dv.ensure(n));
+    CK(dm.ensure(n));
+    CK(mc.ensure(iters + 1));
+    CK(nf.ensure(iters + 1));
+    CK(ni.ensure(iters + 1));
+    CK(cudaMemsetAsync(mc.p, 0, sizeof(unsigned) * (iters + 1), s));
+    CK(cudaMemsetAsync(nf.p, 0, sizeof(int) * (iters + 1), s));
+    CK(cudaMemsetAsync(ni.p, 0, sizeof(unsigned long long) * (iters + 1), s));
+    CK(cudaMemsetAsync(dv.p, 0, n * sizeof(float), s));  // cachedV = 0 (rl.hpp:212)
+    CK(launch_fill_u8(dm.p, 1, n, s));                     // all active; pitch padding stays 1
+    if ((st = h2d(df.p, pitch, f, W, H, s))) return st;
+    CK(cudaMemcpyAsync(du.p, df.p, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    CK(launch_quot_const(df.p, dq.p, W, H, pitch, 0, 1, 0.f, (float)cfg->epsilon_div, s));
+    EventPool ev;
+    CK(ev.make(iters + 1));
+    CK(cudaEventRecord(ev.ev[0], s));
+    const bool dense = fwd->dev.engine == ENG_DENSE;
+    for (int k = 0; k < iters; ++k) {
+        const size_t plane = (size_t)W * H;
+        if (mask_replay) {
+            CK(cudaMemcpy2DAsync(dm.p, pitch, mask_replay + k * plane, W, W, H, cudaMemcpyHostToDevice, s));
+        } else if (k % period == 0) {
+            CK(launch_fill_u8(dm.p, 1, n, s));
+            ctx->launches += 1;
+        }
+        if (mask_record)
+            CK(cudaMemcpy2DAsync(mask_record + k * plane, W, dm.p, pitch, W, H, cudaMemcpyDeviceToHost, s));
+        if (!dense) {
+            CK(launch_count_inactive(dm.p, n, ni.p + k, s));
+            ctx->launches += 1;
+        }
+        Epi e1;
+        e1.mode = EPI_MQUOT;
+        e1.aux = df.p;
+        e1.out2 = dv.p;
+        e1.eps = (float)cfg->epsilon_div;
+        e1.active = dm.p;
+        if (dense) {
+            // compaction (also counts inactive pixels) then the thinned dense pass
+            const DenseTiling t = dense_tiling(W, H);
+            const size_t tiles = (size_t)t.tiles_x * t.tiles_y;
+            CK(fwd->tile_blocks.ensure(tiles * 256));
+            CK(fwd->tile_count.ensure(tiles));
+            CK(launch_tile_compact(dm.p, W, H, pitch, fwd->tile_blocks.p, fwd->tile_count.p, ni.p + k, s));
+            CK(launch_dense(fwd->dev, whole(du.p, dq.p, pitch, W, H), e1, s, fwd->tile_blocks.p, fwd->tile_count.p));
+            ctx->launches += 2;
+        } else if ((st = run_pass(fwd.get(), whole(du.p, dq.p, pitch, W, H), e1, s))) {
+            return st;
+        }
+        Epi e2;
+        e2.mode = EPI_MUPDATE;
+        e2.aux = du.p;
+        e2.clamp = cfg->clamp_nonnegative;
+        e2.maxchange = mc.p + k;
+        e2.nanflag = nf.p + k;
+        e2.active = dm.p;
+        e2.thr = (float)threshold;
+        e2.may_thin = (!mask_replay && k >= thin_start) ? 1 : 0;
+        if (dense) {
+            // the adjoint pass sees the same mask: reuse the forward's lists
+            CK(launch_dense(adj->dev, whole(dq.p, du.p, pitch, W, H), e2, s, fwd->tile_blocks.p, fwd->tile_count.p));
+            ctx->launches += 1;
+        } else if ((st = run_pass(adj.get(), whole(dq.p, du.p, pitch, W, H), e2, s))) {
+            return st;
+        }
+        CK(cudaEventRecord(ev.ev[k + 1], s));
+    }
+    if ((st = d2h(u_out, du.p, pitch, W, H, s))) return st;
+    std::vector<unsigned> hmc(iters + 1);
+    std::vector<int> hnf(iters + 1);
+    std::vector<unsigned long long> hni(iters + 1);
+    CK(cudaMemcpyAsync(hmc.data(), mc.p, sizeof(unsigned) * (iters + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hnf.data(), nf.p, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hni.data(), ni.p, sizeof(unsigned long long) * (iters + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < iters; ++k) {
+        if (hnf[k])
+            return set_err(FDG_ENAN,
+                           "rlDeconvolveSelective: NaN in iterate at iteration " + std::to_string(k + 1));
+        if (trace) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev.ev[k], ev.ev[k + 1]);
+            float m;
+            std::memcpy(&m, &hmc[k], sizeof m);
+            trace[k] = {k + 1, (double)hni[k] / ((double)W * H), (double)m, ms * 1e-3};
+        }
+    }
+    return FDG_OK;
+}
+
+// ------------------------------------------------------------------ solver
+int fdg_solver_create(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, int W, int H, int batch,
+                      fdg_solver** out) {
+    if (!cfg || !out) return set_err(FDG_EINVAL, "null argument");
+    if (W < 1 || H < 1 || batch < 1) return set_err(FDG_EINVAL, "solver: empty input image");
+    if (!(cfg->epsilon_div > 0.0)) return set_err(FDG_EINVAL, "solver: epsilonDiv must be positive");
+    int st = check_device(ctx);
+    if (st) return st;
+    auto s = std::make_unique<fdg_solver>();
+    s->ctx = ctx;
+    s->cfg = *cfg;
+    s->W = W;
+    s->H = H;
+    s->batch = batch;
+    if ((st = make_rl_plans(ctx, desc, cfg->op, &s->fwd, &s->adj))) return st;
+    s->ntrace = std::max(cfg->iterations, 1);
+    CK(s->maxchange.ensure(s->ntrace));
+    CK(s->nanflag.ensure(s->ntrace));
+    CK(cudaMemset(s->maxchange.p, 0, sizeof(unsigned) * s->ntrace));
+    CK(cudaMemset(s->nanflag.p, 0, sizeof(int) * s->ntrace));
+    *out = s.release();
+    return FDG_OK;
+}
+
+void fdg_solver_destroy(fdg_solver* s) { delete s; }
+
+int fdg_solver_reset_trace(fdg_solver* s) {
+    if (!s) return set_err(FDG_EINVAL, "null solver");
+    CK(cudaMemsetAsync(s->maxchange.p, 0, sizeof(unsigned) * s->ntrace, s->ctx->stream));
+    CK(cudaMemsetAsync(s->nanflag.p, 0, sizeof(int) * s->ntrace, s->ctx->stream));
+    return FDG_OK;
+}
+
+int fdg_solver_pass(fdg_solver* s, int pass, const float* d_in, const float* d_aux, float* d_out, int pitch,
+                    long long image_stride, int y0, int y1, int ylo, int yhi, int iteration) {
+    if (!s || !d_in || !d_aux || !d_out) return set_err(FDG_EINVAL, "null argument");
+    if (pitch % 4 || pitch < s->W) return set_err(FDG_EINVAL, "pitch must be a multiple of 4 and >= width");
+    if (ylo > yhi || y0 > y1) return set_err(FDG_EINVAL, "empty row range");
+    Geom g;
+    g.in = d_in;
+    g.out = d_out;
+    g.pitch = pitch;
+    g.W = s->W;
+    g.y0 = y0;
+    g.y1 = y1;
+    g.ylo = ylo;
+    g.yhi = yhi;
+    g.batch = s->batch;
+    g.bstride = image_stride;
+    Epi e;
+    if (pass == 1) {
+        e.mode = EPI_QUOT;
+        e.aux = d_aux;
+        e.eps = (float)s->cfg.epsilon_div;
+        return run_pass(s->fwd.get(), g, e, s->ctx->stream);
+    }
+    if (pass == 2) {
+        const int slot = std::min(std::max(iteration, 0), s->ntrace - 1);
+        e.mode = EPI_UPDATE;
+        e.aux = d_aux;
+        e.clamp = s->cfg.clamp_nonnegative;
+        e.maxchange = s->maxchange.p + slot;
+        e.nanflag = s->nanflag.p + slot;
+        return run_pass(s->adj.get(), g, e, s->ctx->stream);
+    }
+    return set_err(FDG_EINVAL, "pass must be 1 or 2");
+}
+
+int fdg_solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long image_stride, int iterations) {
+    if (!s || !d_f || !d_u) return set_err(FDG_EINVAL, "null argument");
+    if (iterations < 0) return set_err(FDG_EINVAL, "solver: iterations must be >= 0");
+    if (pitch % 4 || pitch < s->W) return set_err(FDG_EINVAL, "pitch must be a multiple of 4 and >= width");
+    if (s->batch > 1 && image_stride < (long long)pitch * s->H) return set_err(FDG_EINVAL, "image_stride too small");
+    const long long stride = s->batch > 1 ? image_stride : (long long)pitch * s->H;
+    const size_t n = (size_t)stride * s->batch;
+    CK(s->q.ensure(n));
+    cudaStream_t st = s->ctx->stream;
+    CK(cudaMemcpyAsync(d_u, d_f, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    for (int k = 0; k < iterations; ++k) {
+        int r = fdg_solver_pass(s, 1, d_u, d_f, s->q.p, pitch, stride, 0, s->H, 0, s->H - 1, k);
+        if (r) return r;
+        r = fdg_solver_pass(s, 2, s->q.p, d_u, d_u, pitch, stride, 0, s->H, 0, s->H - 1, k);
+        if (r) return r;
+    }
+    return FDG_OK;
+}
+
+int fdg_solver_trace(fdg_solver* s, fdg_rl_record* out, int n) {
+    if (!s || !out) return set_err(FDG_EINVAL, "null argument");
+    n = std::min(n, s->ntrace);
+    std::vector<unsigned> mc(n);
+    std::vector<int> nf(n);
+    CK(cudaMemcpyAsync(mc.data(), s->maxchange.p, sizeof(unsigned) * n, cudaMemcpyDeviceToHost, s->ctx->stream));
+    CK(cudaMemcpyAsync(nf.data(), s->nanflag.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s->ctx->stream));
+    CK(cudaStreamSynchronize(s->ctx->stream));
+    for (int k = 0; k < n; ++k) {
+        float m;
+        std::memcpy(&m, &mc[k], sizeof m);
+        out[k] = {k + 1, nf[k] ? 1.0 : 0.0, (double)m, 0.0};  // inactive_fraction slot carries the NaN flag
+    }
+    return FDG_OK;
+}
+
+int fdg_mask_compact(fdg_ctx* ctx, const uint8_t* active, int W, int H, int64_t* idx, int64_t idx_cap,
+                     int64_t* n_active, int32_t* runs, int64_t runs_cap, int64_t* n_runs) {
+    if (!active || W < 1 || H < 1) return set_err(FDG_EINVAL, "empty mask");
+    int st = check_device(ctx);
+    if (st) return st;
+    cudaStream_t s = ctx->stream;
+    const size_t n = (size_t)W * H;
+    DevBuf<uint8_t> dm;
+    DevBuf<int> counts;
+    DevBuf<long long> ro, ao;
+    CK(dm.ensure(n));
+    CK(counts.ensure(2 * (size_t)H));
+    CK(ro.ensure(H));
+    CK(ao.ensure(H));
+    CK(cudaMemcpyAsync(dm.p, active, n, cudaMemcpyHostToDevice, s));
+    CK(launch_row_runs(dm.p, W, H, counts.p, s));
+    std::vector<int> hc(2 * (size_t)H);
+    CK(cudaMemcpyAsync(hc.data(), counts.p, hc.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<long long> hro(H), hao(H);
+    long long tr = 0, ta = 0;
+    for (int y = 0; y < H; ++y) {
+        hro[y] = tr;
+        hao[y] = ta;
+        tr += hc[2 * y];
+        ta += hc[2 * y + 1];
+    }
+    if (n_runs) *n_runs = tr;
+    if (n_active) *n_active = ta;
+    const bool want_runs = runs && runs_cap >= tr, want_idx = idx && idx_cap >= ta;
+    if (!want_runs && !want_idx) return FDG_OK;
+    DevBuf<int32_t> druns;
+    DevBuf<int64_t> didx;
+    if (want_runs) CK(druns.ensure(3 * (size_t)tr + 1));
+    if (want_idx) CK(didx.ensure((size_t)ta + 1));
+    CK(cudaMemcpyAsync(ro.p, hro.data(), H * sizeof(long long), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ao.p, hao.data(), H * sizeof(long long), cudaMemcpyHostToDevice, s));
+    CK(launch_row_runs_emit(dm.p, W, H, ro.p, ao.p, want_runs ? druns.p : nullptr, want_idx ? didx.p : nullptr, s));
+    ctx->launches += 2;
+    if (want_runs) CK(cudaMemcpyAsync(runs, druns.p, 3 * (size_t)tr * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (want_idx) CK(cudaMemcpyAsync(idx, didx.p, (size_t)ta * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return FDG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// internal.h -- shared declarations of libfdgpu (host plan logic + kernel
+// launchers).  Not part of the ABI; see include/fdgpu.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "fdgpu.h"
+
+namespace fdg {
+
+// ---------------------------------------------------------------- host PSF
+struct Tap {
+    int dx, dy;
+    double w;
+};
+struct Span {
+    int dy, xmin, xmax;
+};
+
+// A restated Psf variant (psf.hpp:173) built from an fdg_psf_desc.
+struct HostPsf {
+    int repr = FDG_PSF_DENSE;
+    int w = 0, h = 0, ax = 0, ay = 0;  // DensePsf
+    std::vector<double> weights;
+    std::vector<Span> rows;  // UniformConvexPsf
+    std::vector<Tap> taps;   // SparsePsf
+};
+
+struct LineShape {
+    int length, min_dx, dy;
+};
+struct RectShape {
+    int mx, my, min_dx, min_dy;
+};
+
+// psf.hpp restatement used by the plan builder (plan.cpp)
+bool psf_from_desc(const fdg_psf_desc* d, HostPsf* out, std::string* err);
+HostPsf psf_adjoint(const HostPsf& p);
+std::vector<Tap> psf_taps(const HostPsf& p);  // toSparse order
+bool psf_as_line(const HostPsf& p, LineShape* out);
+bool psf_as_rect(const HostPsf& p, RectShape* out);
+bool psf_as_convex(const HostPsf& p, std::vector<Span>* out);
+bool psf_accepts(int kind, const HostPsf& p);
+int psf_dispatch(const HostPsf& p, int preference, std::string* err);  // -1 on error
+const char* op_name(int kind);
+
+// ------------------------------------------------------------ device plan
+enum Engine { ENG_RECT = 0, ENG_SPANS = 1, ENG_DENSE = 2, ENG_TAPS = 3, ENG_CYCLIC = 4 };
+
+struct DevPsf {
+    int engine = ENG_TAPS;
+    int min_dx = 0, max_dx = 0, min_dy = 0, max_dy = 0;  // tap extents
+    int mx = 1, my = 1;                                  // rect engine
+    int uniform = 0;
+    float scale = 1.f;  // uniform weight (1/count) or 1
+    int nrows = 0, ntaps = 0;
+    int* d_row_start = nullptr;  // [nrows+1], rows r = dy - min_dy
+    int* d_dx = nullptr;         // [ntaps]
+    float* d_w = nullptr;        // [ntaps]
+    int* d_span = nullptr;       // [2*nrows] xmin,xmax per row (spans engine)
+    int mw = 0, mh = 0, mwp = 0;  // dense engine: grid, padded width
+    float* d_dense = nullptr;     // [mh * mwp]
+};
+
+enum EpiMode {
+    EPI_STORE = 0,    // out = v
+    EPI_QUOT = 1,     // out = aux / max(v, eps)
+    EPI_UPDATE = 2,   // out = clamp(v * aux); max|out-aux|, NaN
+    EPI_MQUOT = 3,    // masked fwd: active: out2(cachedV) = v, out = aux / max(v, eps)
+    EPI_MUPDATE = 4,  // masked adj: active: as UPDATE + deactivate when |du| < thr
+};
+
+struct Epi {
+    int mode = EPI_STORE;
+    const float* aux = nullptr;
+    float* out2 = nullptr;
+    float eps = 1e-8f;
+    int clamp = 1;
+    unsigned* maxchange = nullptr;  // float bits, atomicMax
+    int* nanflag = nullptr;
+    uint8_t* active = nullptr;      // masked modes / masked store
+    float thr = 0.f;
+    int may_thin = 0;
+};
+
+struct Geom {
+    const float* in = nullptr;
+    float* out = nullptr;
+    int pitch = 0;
+    int W = 0;
+    int y0 = 0, y1 = 0;    // output rows [y0, y1)
+    int ylo = 0, yhi = 0;  // readable input rows (inclusive clamp range)
+    int batch = 1;
+    long long bstride = 0;  // elements between images
+    int wrap = 0;           // cyclic boundary (Fourier contract)
+};
+
+// kernel launchers (return cudaError_t of the launch)
+cudaError_t launch_rect(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st);
+cudaError_t launch_taps(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st);
+cudaError_t launch_dense(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st,
+                         const int* d_tile_blocks, const int* d_tile_count);
+cudaError_t launch_spans(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st);
+bool spans_supported(const DevPsf& p);
+bool dense_supported(const DevPsf& p);
+
+// compaction (kernels_mask.cu)
+struct DenseTiling {
+    int tiles_x, tiles_y;
+};
+DenseTiling dense_tiling(int W, int H);
+cudaError_t launch_tile_compact(const uint8_t* active, int W, int H, int pitch_mask,
+                                int* d_tile_blocks, int* d_tile_count,
+                                unsigned long long* d_inactive, cudaStream_t st);
+cudaError_t launch_fill_u8(uint8_t* p, uint8_t v, size_t n, cudaStream_t st);
+cudaError_t launch_row_runs(const uint8_t* active, int W, int H, int* d_counts, cudaStream_t st);
+cudaError_t launch_row_runs_emit(const uint8_t* active, int W, int H, const long long* d_run_off,
+                                 const long long* d_act_off, int32_t* d_runs, int64_t* d_idx,
+                                 cudaStream_t st);
+cudaError_t launch_quot_const(const float* f, float* q, int W, int H, int pitch, long long bstride, int batch,
+                              float c, float eps, cudaStream_t st);
+bool rect_supported(int mx);
+cudaError_t launch_count_inactive(const uint8_t* active, size_t n, unsigned long long* out,
+                                  cudaStream_t st);
+
+}  // namespace fdg

@@ -1,0 +1,171 @@
+// kernels_mask.cu -- stream compaction for selective (thinned) RL.
+//
+// k_tile_compact: one CTA per 64x64 dense tile; each thread owns a 4x4 pixel
+//   block, flags it when any pixel is active, and the CTA compacts the
+//   flagged block ids in ascending (row-major) order with warp ballots +
+//   popc prefix sums.  The thinned dense kernel consumes these per-tile lists
+//   (tiles with no active block exit immediately).  The same pass counts the
+//   inactive pixels of the iteration for RlTrace.inactiveFraction.
+// k_row_count / k_row_emit: the reference's row-major run walk
+//   (convolve.hpp:450-465) on the device, one thread per row, emitting the
+//   ordered active index list and (y, x0, len) runs for bit-exact checks.
+#include "common.cuh"
+
+namespace fdg {
+namespace {
+
+constexpr int TD = 64;
+
+__global__ void __launch_bounds__(256) k_tile_compact(const uint8_t* act, int W, int H, int pitch,
+                                                      int* tile_blocks, int* tile_count,
+                                                      unsigned long long* inactive) {
+    __shared__ int warp_n[8];
+    __shared__ unsigned long long warp_inact[8];
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    const int bx = t & 15, by = t >> 4;
+    const int x0 = blockIdx.x * TD + 4 * bx, y0 = blockIdx.y * TD + 4 * by;
+    int any = 0, nin = 0;
+    for (int i = 0; i < 4; ++i) {
+        const int y = y0 + i;
+        if (y >= H) break;
+        for (int j = 0; j < 4; ++j) {
+            const int x = x0 + j;
+            if (x >= W) break;
+            const int a = act[(long long)y * pitch + x];
+            any |= a;
+            nin += !a;
+        }
+    }
+    const unsigned ball = __ballot_sync(0xffffffffu, any);
+    const int cnt_inact = __reduce_add_sync(0xffffffffu, nin);
+    if (lane == 0) {
+        warp_n[wid] = __popc(ball);
+        warp_inact[wid] = (unsigned long long)cnt_inact;
+    }
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < wid; ++w) base += warp_n[w];
+    if (any) tile_blocks[(long long)tile * 256 + base + __popc(ball & ((1u << lane) - 1u))] = t;
+    if (t == 0) {
+        int total = 0;
+        unsigned long long ni = 0;
+        for (int w = 0; w < 8; ++w) {
+            total += warp_n[w];
+            ni += warp_inact[w];
+        }
+        tile_count[tile] = total;
+        if (inactive && ni) atomicAdd(inactive, ni);
+    }
+}
+
+__global__ void k_fill_u8(uint8_t* p, uint8_t v, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+__global__ void k_count_zero(const uint8_t* p, size_t n, unsigned long long* out) {
+    unsigned long long c = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        c += p[i] == 0;
+    c = __reduce_add_sync(0xffffffffu, (unsigned)c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// per row: [0] = number of active runs, [1] = number of active pixels
+__global__ void k_row_count(const uint8_t* act, int W, int H, int* counts) {
+    const int y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= H) return;
+    const uint8_t* r = act + (long long)y * W;
+    int runs = 0, n = 0, prev = 0;
+    for (int x = 0; x < W; ++x) {
+        const int a = r[x] != 0;
+        runs += a && !prev;
+        n += a;
+        prev = a;
+    }
+    counts[2 * y] = runs;
+    counts[2 * y + 1] = n;
+}
+
+__global__ void k_row_emit(const uint8_t* act, int W, int H, const long long* run_off, const long long* act_off,
+                           int32_t* runs, int64_t* idx) {
+    const int y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (y >= H) return;
+    const uint8_t* r = act + (long long)y * W;
+    long long ro = run_off[y], ao = act_off[y];
+    int x = 0;
+    while (x < W) {  // the run walk of convolve.hpp:450-465
+        int end = x + 1;
+        if (r[x]) {
+            while (end < W && r[end]) ++end;
+            if (runs) {
+                runs[3 * ro] = y;
+                runs[3 * ro + 1] = x;
+                runs[3 * ro + 2] = end - x;
+            }
+            ++ro;
+            if (idx)
+                for (int i = x; i < end; ++i) idx[ao++] = (int64_t)y * W + i;
+        } else {
+            while (end < W && !r[end]) ++end;
+        }
+        x = end;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_tile_compact(const uint8_t* active, int W, int H, int pitch_mask, int* d_tile_blocks,
+                                int* d_tile_count, unsigned long long* d_inactive, cudaStream_t st) {
+    const DenseTiling t = dense_tiling(W, H);
+    k_tile_compact<<<dim3(t.tiles_x, t.tiles_y), 256, 0, st>>>(active, W, H, pitch_mask, d_tile_blocks,
+                                                               d_tile_count, d_inactive);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_u8(uint8_t* p, uint8_t v, size_t n, cudaStream_t st) {
+    k_fill_u8<<<1184, 256, 0, st>>>(p, v, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_count_inactive(const uint8_t* active, size_t n, unsigned long long* out, cudaStream_t st) {
+    k_count_zero<<<1184, 256, 0, st>>>(active, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_runs(const uint8_t* active, int W, int H, int* d_counts, cudaStream_t st) {
+    k_row_count<<<(H + 127) / 128, 128, 0, st>>>(active, W, H, d_counts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_runs_emit(const uint8_t* active, int W, int H, const long long* d_run_off,
+                                 const long long* d_act_off, int32_t* d_runs, int64_t* d_idx, cudaStream_t st) {
+    k_row_emit<<<(H + 127) / 128, 128, 0, st>>>(active, W, H, d_run_off, d_act_off, d_runs, d_idx);
+    return cudaGetLastError();
+}
+
+}  // namespace fdg
+
+namespace fdg {
+namespace {
+// q = f / max(c, eps) over a pitched batch (selective RL start: cachedV = 0,
+// so every pixel's quotient is defined before the first masked pass)
+__global__ void k_quot_const(const float* f, float* q, int W, int H, int pitch, long long bstride, int batch,
+                             float c, float eps) {
+    const long long n = (long long)W * H * batch;
+    const float d = c < eps ? eps : c;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long b = i / ((long long)W * H), r = i - b * W * H;
+        const long long idx = b * bstride + (r / W) * pitch + (r % W);
+        q[idx] = f[idx] / d;
+    }
+}
+}  // namespace
+
+cudaError_t launch_quot_const(const float* f, float* q, int W, int H, int pitch, long long bstride, int batch,
+                              float c, float eps, cudaStream_t st) {
+    k_quot_const<<<1184, 256, 0, st>>>(f, q, W, H, pitch, bstride, batch, c, eps);
+    return cudaGetLastError();
+}
+}  // namespace fdg

@@ -1,0 +1,210 @@
+"""Richardson-Lucy drivers on the B200 -- Python face of
+/root/reference/proj/include/fastdeconv/rl.hpp.
+
+``rlDeconvolve`` / ``rlDeconvolveSelective`` / ``rlStep`` keep the reference
+signatures and error behaviour; the whole iteration loop runs inside
+libfdgpu with u, f and q resident in HBM (two fused passes per iteration,
+see paper_1304_7211_b200/csrc/fdgpu.cu).  ``RlSolver`` is the device-resident
+form used by bench.py and the row-strip sharding (torch tensors in, no host
+copies inside the loop).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import Context, Desc, RlConfigC, RlRecordC, check, f32, fptr, lib, u8ptr
+from .convolve import OperatorKind, convolve
+
+
+@dataclass
+class RlConfig:
+    """rl.hpp:18-23"""
+
+    iterations: int = 100
+    op: OperatorKind = OperatorKind.Auto
+    epsilonDiv: float = 1e-8
+    clampNonNegative: bool = True
+
+    def c(self) -> RlConfigC:
+        return RlConfigC(int(self.iterations), int(self.op), float(self.epsilonDiv), int(bool(self.clampNonNegative)))
+
+
+@dataclass
+class RlIterationRecord:
+    """rl.hpp:25-30"""
+
+    iteration: int = 0
+    inactiveFraction: float = 0.0
+    maxAbsChange: float = 0.0
+    seconds: float = 0.0
+
+
+@dataclass
+class RlTrace:
+    """rl.hpp:32-50"""
+
+    records: List[RlIterationRecord] = field(default_factory=list)
+
+    def omittedPercent(self) -> float:
+        if not self.records:
+            return 0.0
+        s = 0.0
+        for r in self.records:
+            s += r.inactiveFraction
+        return 100.0 * s / len(self.records)
+
+    def totalSeconds(self) -> float:
+        s = 0.0
+        for r in self.records:
+            s += r.seconds
+        return s
+
+
+@dataclass
+class RlResult:
+    """rl.hpp:52-55 (+ the recorded masks of a selective run when asked)"""
+
+    image: np.ndarray
+    trace: RlTrace
+    masks: Optional[np.ndarray] = None
+
+
+class BoundaryMode(enum.IntEnum):
+    """rl.hpp:67"""
+
+    Cyclic = 0
+    Replicate = 1
+
+
+def _image(f) -> np.ndarray:
+    a = np.asarray(f)
+    if a.ndim != 2:
+        raise _lib.FdgInvalidArgument("empty input image")
+    return a
+
+
+def _trace(recs, n) -> RlTrace:
+    return RlTrace([RlIterationRecord(recs[i].iteration, recs[i].inactive_fraction, recs[i].max_abs_change,
+                                      recs[i].seconds) for i in range(n)])
+
+
+def _out(a, u32):
+    return u32.astype(a.dtype if a.dtype in (np.float32, np.float64) else np.float64, copy=False)
+
+
+def rlDeconvolve(f, h, cfg: RlConfig = RlConfig(), ctx: Optional[Context] = None) -> RlResult:
+    """Standard RL from u0 = f (rl.hpp:140-179)."""
+    a = _image(f)
+    src = f32(a)
+    hh, w = src.shape if src.size else (0, 0)
+    u = np.empty_like(src)
+    n = max(cfg.iterations, 0)
+    recs = (RlRecordC * max(n, 1))()
+    c = cfg.c()
+    check(lib().fdg_rl_deconvolve(Context.handle_or_null(ctx), Desc(h).ref, C.byref(c), fptr(src), w, hh, fptr(u), recs))
+    return RlResult(_out(a, u), _trace(recs, n))
+
+
+def rlDeconvolveSelective(f, h, cfg: RlConfig, threshold: float, period: int = 10, thin_start: int = 0,
+                          mask_replay: Optional[np.ndarray] = None, record_masks: bool = False,
+                          ctx: Optional[Context] = None) -> RlResult:
+    """Selective (thinned) RL, rl.hpp:187-257.  ``thin_start`` holds the
+    deactivation off for 0-based iterations k < thin_start (0 = reference);
+    ``mask_replay`` (iterations x H x W uint8) replays recorded active masks."""
+    a = _image(f)
+    src = f32(a)
+    hh, w = src.shape
+    u = np.empty_like(src)
+    n = max(cfg.iterations, 0)
+    recs = (RlRecordC * max(n, 1))()
+    rep = None
+    if mask_replay is not None:
+        rep = np.ascontiguousarray(mask_replay, dtype=np.uint8)
+        if rep.shape != (n, hh, w):
+            raise _lib.FdgInvalidArgument("mask_replay must be iterations x height x width")
+    rec = np.zeros((n, hh, w), dtype=np.uint8) if record_masks else None
+    c = cfg.c()
+    check(lib().fdg_rl_deconvolve_selective(Context.handle_or_null(ctx), Desc(h).ref, C.byref(c), float(threshold), int(period),
+                                            int(thin_start), u8ptr(rep), u8ptr(rec), fptr(src), w, hh,
+                                            fptr(u), recs))
+    return RlResult(_out(a, u), _trace(recs, n), rec)
+
+
+def rlStep(u, f, h, cfg: RlConfig = RlConfig(), ctx: Optional[Context] = None) -> np.ndarray:
+    """One multiplicative update (rl.hpp:131-137)."""
+    ua, fa = _image(u), _image(f)
+    if ua.shape != fa.shape:
+        raise _lib.FdgInvalidArgument("rlStep: image dimensions differ")
+    u32, f32_ = f32(ua), f32(fa)
+    out = np.empty_like(u32)
+    hh, w = u32.shape
+    c = cfg.c()
+    mc = C.c_double(0)
+    check(lib().fdg_rl_step(Context.handle_or_null(ctx), Desc(h).ref, C.byref(c), fptr(u32), fptr(f32_), w, hh, fptr(out), C.byref(mc)))
+    return _out(ua, out)
+
+
+def blurImage(g, h, mode: BoundaryMode) -> np.ndarray:
+    """rl.hpp:261-265: cyclic = the Fourier operator's wrap-around contract,
+    replicate = the auto-dispatched spatial operator."""
+    if BoundaryMode(mode) == BoundaryMode.Cyclic:
+        return convolve(g, h, OperatorKind.Fourier)
+    return convolve(g, h, OperatorKind.Auto)
+
+
+class RlSolver:
+    """Device-resident RL for ``batch`` images of ``height`` x ``width``
+    (fdg_solver_*).  Buffers are torch CUDA tensors (float32, last dim =
+    pitch, pitch % 4 == 0); work is issued on torch's current stream."""
+
+    def __init__(self, h, cfg: RlConfig, width: int, height: int, batch: int = 1, device: int = 0,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or Context(device)
+        self.cfg = cfg
+        self.width, self.height, self.batch = width, height, batch
+        s = C.c_void_p()
+        c = cfg.c()
+        check(lib().fdg_solver_create(self.ctx.h, Desc(h).ref, C.byref(c), width, height, batch, C.byref(s)))
+        self.h = s
+
+    def use_stream(self, stream_ptr: int):
+        self.ctx.set_stream(stream_ptr)
+
+    def run(self, f, u, iterations: Optional[int] = None):
+        """u <- f, then `iterations` RL iterations in place (device tensors)."""
+        it = self.cfg.iterations if iterations is None else iterations
+        pitch = f.shape[-1]
+        stride = f.stride(0) if f.dim() == 3 else pitch * self.height
+        check(lib().fdg_solver_run(self.h, C.c_void_p(f.data_ptr()), C.c_void_p(u.data_ptr()), pitch, stride, it))
+
+    def pass_(self, which: int, d_in: int, d_aux: int, d_out: int, pitch: int, image_stride: int, y0: int,
+              y1: int, ylo: int, yhi: int, iteration: int):
+        """One fused pass on raw device pointers (row-strip sharding)."""
+        check(lib().fdg_solver_pass(self.h, which, C.c_void_p(d_in), C.c_void_p(d_aux), C.c_void_p(d_out), pitch,
+                                    image_stride, y0, y1, ylo, yhi, iteration))
+
+    def trace(self, n: Optional[int] = None):
+        """[(max|du|, nan_flag)] per iteration (synchronises)."""
+        n = n or max(self.cfg.iterations, 1)
+        recs = (RlRecordC * n)()
+        check(lib().fdg_solver_trace(self.h, recs, n))
+        return [(recs[i].max_abs_change, bool(recs[i].inactive_fraction)) for i in range(n)]
+
+    def reset_trace(self):
+        check(lib().fdg_solver_reset_trace(self.h))
+
+    def launches(self) -> int:
+        return self.ctx.launch_count()
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().fdg_solver_destroy(self.h)
+        except Exception:
+            pass
