@@ -1,0 +1,139 @@
+"""Multi-GPU Richardson-Lucy: row-strip sharding of one large image with a
+per-iteration PSF-radius halo exchange, and by-image sharding of batches
+(SURVEY 8e).  One process per GPU, torch.distributed for the plumbing
+(NCCL over NVLink on the B200 box; gloo on CPU for the tests).
+
+Row strips.  Rank r owns rows [r*H/P, (r+1)*H/P).  Every plane (f, u, q)
+is stored with T halo rows above and below the core (T = the PSF's
+vertical radius), the device pointer addressing core row 0.  Per iteration:
+
+    exchange(u)   top/bottom T core rows <-> neighbours' halos
+    pass 1        q = f / max(h (x) u, eps)       rows [0, core), reads [ylo, yhi]
+    exchange(q)
+    pass 2        u = max(h* (x) q * u, 0)
+
+Replicate clamping happens only at the global first/last row (ylo = 0 on
+rank 0, yhi = core-1 on the last rank); interior strip edges read the
+neighbour's rows, so the sharded result equals the single-GPU one (up to
+the box2d vertical running-sum order).  The halo exchange is the path's
+only collective; batches need none.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, List, Optional
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass
+class Strip:
+    rank: int
+    world: int
+    height: int      # global rows
+    r0: int          # first global row of the core
+    core: int        # core rows
+    halo: int        # T
+
+    @property
+    def ylo(self) -> int:
+        return -self.halo if self.rank > 0 else 0
+
+    @property
+    def yhi(self) -> int:
+        return self.core - 1 + (self.halo if self.rank < self.world - 1 else 0)
+
+    @property
+    def rows(self) -> int:
+        return self.core + 2 * self.halo
+
+
+def strip_of(height: int, world: int, rank: int, halo: int) -> Strip:
+    r0 = rank * height // world
+    r1 = (rank + 1) * height // world
+    if world > 1 and r1 - r0 < halo:
+        raise ValueError(f"strip of {r1 - r0} rows is thinner than the {halo}-row halo")
+    return Strip(rank, world, height, r0, r1 - r0, halo)
+
+
+def psf_halo(psf) -> int:
+    from .psf import taps_of
+    dys = [t[1] for t in taps_of(psf)]
+    return max(0, -min(dys), max(dys))
+
+
+def exchange(buf: torch.Tensor, s: Strip, group=None):
+    """Swap T boundary core rows with rank-1 / rank+1 (no wrap-around).
+    buf: (rows, pitch) with the core at rows [T, T + core)."""
+    if s.world == 1 or s.halo == 0:
+        return
+    T, c = s.halo, s.core
+    ops = []
+    if s.rank > 0:
+        ops.append(dist.P2POp(dist.isend, buf[T:2 * T], s.rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, buf[0:T], s.rank - 1, group))
+    if s.rank < s.world - 1:
+        ops.append(dist.P2POp(dist.isend, buf[c:c + T], s.rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, buf[T + c:T + c + T], s.rank + 1, group))
+    for r in dist.batch_isend_irecv(ops):
+        r.wait()
+
+
+class GpuPasses:
+    """Fused passes on the device through libfdgpu (RlSolver.pass_)."""
+
+    def __init__(self, solver):
+        self.solver = solver
+
+    def __call__(self, which: int, src: torch.Tensor, aux: torch.Tensor, out: torch.Tensor, s: Strip, k: int):
+        pitch = src.shape[-1]
+        off = s.halo * pitch * 4
+        self.solver.pass_(which, src.data_ptr() + off, aux.data_ptr() + off, out.data_ptr() + off, pitch,
+                          s.rows * pitch, 0, s.core, s.ylo, s.yhi, k)
+
+
+def rl_strips(f_local: torch.Tensor, s: Strip, iterations: int, passes: Callable, group=None,
+              u: Optional[torch.Tensor] = None, q: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """RL on this rank's strip.  f_local: (rows, pitch) with halos (f's halo
+    rows are never read).  Returns u (same layout)."""
+    if u is None:
+        u = torch.empty_like(f_local)
+    if q is None:
+        q = torch.empty_like(f_local)
+    u.copy_(f_local)
+    for k in range(iterations):
+        exchange(u, s, group)
+        passes(1, u, f_local, q, s, k)
+        exchange(q, s, group)
+        passes(2, q, u, u, s, k)
+    return u
+
+
+def load_strip(f_global, s: Strip, pitch: int, device=None, dtype=torch.float32) -> torch.Tensor:
+    """This rank's rows of a (H, W) host array into a (rows, pitch) buffer."""
+    import numpy as np
+    buf = torch.zeros((s.rows, pitch), dtype=dtype)
+    w = f_global.shape[1]
+    buf[s.halo:s.halo + s.core, :w] = torch.from_numpy(np.ascontiguousarray(f_global[s.r0:s.r0 + s.core]))
+    return buf.to(device) if device is not None else buf
+
+
+def gather_strips(u: torch.Tensor, s: Strip, width: int, group=None) -> Optional[torch.Tensor]:
+    """Concatenate every rank's core rows on rank 0 (tests / validation)."""
+    core = u[s.halo:s.halo + s.core, :width].contiguous()
+    sizes = [None] * s.world
+    dist.all_gather_object(sizes, core.shape[0], group=group)
+    mx = max(sizes)
+    pad = torch.zeros((mx, width), dtype=u.dtype, device=u.device)
+    pad[:core.shape[0]] = core
+    out = [torch.zeros_like(pad) for _ in range(s.world)]
+    dist.all_gather(out, pad, group=group)
+    if s.rank != 0:
+        return None
+    return torch.cat([o[:n] for o, n in zip(out, sizes)], dim=0)
+
+
+def batch_share(batch: int, world: int, rank: int) -> range:
+    """Images of a batch owned by `rank` (by-image sharding, no collective)."""
+    return range(rank * batch // world, (rank + 1) * batch // world)

@@ -1,0 +1,95 @@
+"""Row-strip sharding host logic on CPU: world_size 2 over gloo, the fused
+passes evaluated by the oracle on each rank's strip + halo.  The gathered
+result must equal the single-image oracle run (the halo exchange and the
+clamp ranges are exactly right iff this holds; SURVEY 8c strip-parallel
+oracle).  The GPU executor (GpuPasses) runs the same driver on the box."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import pyoracle as O
+from paper_1304_7211_b200 import sharded as S
+from paper_1304_7211_b200.psf import adjoint, makeBoxPsf, makeDiscPsf, makeLinePsf
+from paper_1304_7211_b200 import workloads as W
+
+
+class OraclePasses:
+    def __init__(self, psf, op, eps=1e-8):
+        self.psf, self.adj, self.op, self.eps = psf, adjoint(psf), op, eps
+
+    def __call__(self, which, src, aux, out, s, k):
+        T, w = s.halo, self.width
+        img = src[T + s.ylo:T + s.yhi + 1, :w].numpy()
+        conv = O.convolve(img, self.psf if which == 1 else self.adj, self.op)
+        v = conv[-s.ylo:-s.ylo + s.core]
+        a = aux[T:T + s.core, :w].numpy()
+        if which == 1:
+            res = a / np.where(v < self.eps, self.eps, v)
+        else:
+            res = np.maximum(v * a, 0.0)
+        out[T:T + s.core, :w] = torch.from_numpy(res)
+
+
+def _worker(rank, world, port, case, H, W_, it, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        psf, op = CASES[case]()
+        rng = np.random.default_rng(9)
+        f = rng.random((H, W_)) + 0.05
+        s = S.strip_of(H, world, rank, S.psf_halo(psf))
+        fl = S.load_strip(f, s, W_ + 3, dtype=torch.float64)
+        ex = OraclePasses(psf, op)
+        ex.width = W_
+        u = S.rl_strips(fl, s, it, ex)
+        full = S.gather_strips(u, s, W_)
+        if rank == 0:
+            ref, _, _ = O.rl_deconvolve(f, psf, it, op)
+            q.put(float(np.max(np.abs(full.numpy() - ref) / ref)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+CASES = {
+    "disc5-generic": lambda: (makeDiscPsf(5), O.GENERIC_BOX),
+    "box3x5-box2d": lambda: (makeBoxPsf(3, 5), O.BOX2D_SLIDING),
+    "gauss-naive": lambda: (W.gaussian31(seed=5, size=7), O.NAIVE),
+    "line9-box1d": lambda: (makeLinePsf(9), O.BOX1D_SLIDING),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_two_rank_strips_equal_single_image(name):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, 37, 23, 6, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    err = q.get(timeout=5)
+    assert err < 1e-12, err
+
+
+def test_strip_geometry():
+    s0, s1, s2 = (S.strip_of(100, 3, r, 7) for r in range(3))
+    assert (s0.r0, s0.core, s0.ylo, s0.yhi) == (0, 33, 0, 39)
+    assert (s1.r0, s1.core, s1.ylo, s1.yhi) == (33, 33, -7, 39)
+    assert (s2.r0, s2.core, s2.ylo, s2.yhi) == (66, 34, -7, 33)
+    assert list(S.batch_share(64, 8, 3)) == list(range(24, 32))
+    with pytest.raises(ValueError):
+        S.strip_of(10, 4, 0, 7)
