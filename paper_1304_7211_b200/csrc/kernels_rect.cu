@@ -13,6 +13,8 @@
 // epilogue (quotient or multiplicative update + max|du| + NaN flag) before a
 // float4 store.  HBM traffic per pass: one read of the conv input, one read
 // of the epilogue operand, one write (12 B/px), plus (my-1)/band halo rows.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace fdg {
@@ -86,11 +88,12 @@ __device__ __forceinline__ void hsum_fast(const float* seg_row, int t, float (&H
     hsum4<MX, OFF, 4 * NCH>(v, H);
 }
 
-template <int MODE, int MX>
+template <int MODE, int MX, int R>
 __global__ void __launch_bounds__(NT + 32) k_rect(const RectArgs a) {
+    constexpr int SS = S / R;  // stages of R rows (S rows in flight)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-    uint64_t* empty = full + S;
+    uint64_t* empty = full + SS;
     float* in_ring = reinterpret_cast<float*>(smem_raw + 128);
     float* aux_ring = in_ring + S * a.seg;
     float4* hring = reinterpret_cast<float4*>(aux_ring + S * CW);
@@ -106,7 +109,7 @@ __global__ void __launch_bounds__(NT + 32) k_rect(const RectArgs a) {
     constexpr bool HAS_AUX = MODE != EPI_STORE;
 
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
+        for (int s = 0; s < SS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NT / 32);
         }
@@ -122,18 +125,22 @@ __global__ void __launch_bounds__(NT + 32) k_rect(const RectArgs a) {
             const unsigned in_bytes = (unsigned)(c1 - c0) * 4u;
             const int dst_off = c0 - (x0 - a.HL);
             const unsigned aux_bytes = (unsigned)(min(a.Wp4, x0 + CW) - x0) * 4u;
-            for (int i = 0; i < steps; ++i) {
-                const int s = i % S;
-                if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
-                const int row = clampi(yb0 + a.min_dy + i, a.ylo, a.yhi);
-                const bool aux_now = HAS_AUX && i >= my - 1;
-                mbar_arrive_expect_tx(&full[s], in_bytes + (aux_now ? aux_bytes : 0u));
-                bulk_g2s(in_ring + (size_t)s * a.seg + dst_off, a.in + img + (long long)row * a.pitch + c0,
-                         in_bytes, &full[s]);
-                if (aux_now) {
-                    const int yo = yb0 + i - (my - 1);
-                    bulk_g2s(aux_ring + (size_t)s * CW, a.aux + img + (long long)yo * a.pitch + x0, aux_bytes,
-                             &full[s]);
+            for (int i0 = 0, st = 0; i0 < steps; i0 += R, ++st) {
+                const int s = st % SS;
+                if (st >= SS) mbar_wait(&empty[s], ((st / SS) - 1) & 1);
+                const int nr = min(R, steps - i0);
+                const int naux = HAS_AUX ? max(0, min(nr, i0 + nr - (my - 1))) : 0;
+                mbar_arrive_expect_tx(&full[s], nr * in_bytes + naux * aux_bytes);
+                for (int r = 0; r < nr; ++r) {
+                    const int i = i0 + r;
+                    const int row = clampi(yb0 + a.min_dy + i, a.ylo, a.yhi);
+                    bulk_g2s(in_ring + (size_t)(s * R + r) * a.seg + dst_off, a.in + img + (long long)row * a.pitch + c0,
+                             in_bytes, &full[s]);
+                    if (HAS_AUX && i >= my - 1) {
+                        const int yo = yb0 + i - (my - 1);
+                        bulk_g2s(aux_ring + (size_t)(s * R + r) * CW, a.aux + img + (long long)yo * a.pitch + x0,
+                                 aux_bytes, &full[s]);
+                    }
                 }
             }
         }
@@ -150,10 +157,14 @@ __global__ void __launch_bounds__(NT + 32) k_rect(const RectArgs a) {
     TraceAcc tr;
     int slot = 0;
 
-    for (int i = 0; i < steps; ++i) {
-        const int s = i % S;
-        mbar_wait(&full[s], (i / S) & 1);
-        const float* seg = in_ring + (size_t)s * a.seg;
+    for (int i0 = 0, st = 0; i0 < steps; i0 += R, ++st) {
+      const int s = st % SS;
+      mbar_wait(&full[s], (st / SS) & 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = i0 + r;
+        if (i >= steps) break;
+        const float* seg = in_ring + (size_t)(s * R + r) * a.seg;
         float H[4];
         if (interior) {
             const float* base = seg + 4 * k0;
@@ -209,31 +220,31 @@ __global__ void __launch_bounds__(NT + 32) k_rect(const RectArgs a) {
             const int yo = yb0 + i - (my - 1);
             const long long rowoff = img + (long long)yo * a.pitch;
             float v[4] = {col.x * a.scale, col.y * a.scale, col.z * a.scale, col.w * a.scale};
-            float r[4];
-            const float* ax = aux_ring + (size_t)s * CW + 4 * tid;
+            float res[4];
+            const float* ax = aux_ring + (size_t)(s * R + r) * CW + 4 * tid;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (MODE == EPI_STORE) {
-                    r[j] = v[j];
+                    res[j] = v[j];
                 } else if (MODE == EPI_QUOT) {
-                    const float d = v[j] < a.e.eps ? a.e.eps : v[j];
-                    r[j] = ax[j] / d;
+                    res[j] = div_fast(ax[j], v[j] < a.e.eps ? a.e.eps : v[j]);
                 } else {  // EPI_UPDATE
                     const float u = ax[j];
                     float value = v[j] * u;
                     if (a.e.clamp && value < 0.f) value = 0.f;
                     if (xc + j < a.W) tr.add(fabsf(value - u), value);
-                    r[j] = value;
+                    res[j] = value;
                 }
             }
             if (xc + 3 < a.W) {
-                *reinterpret_cast<float4*>(a.out + rowoff + xc) = make_float4(r[0], r[1], r[2], r[3]);
+                *reinterpret_cast<float4*>(a.out + rowoff + xc) = make_float4(res[0], res[1], res[2], res[3]);
             } else {
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    if (xc + j < a.W) a.out[rowoff + xc + j] = r[j];
+                    if (xc + j < a.W) a.out[rowoff + xc + j] = res[j];
             }
         }
+      }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
@@ -242,7 +253,11 @@ __global__ void __launch_bounds__(NT + 32) k_rect(const RectArgs a) {
 
 template <int MODE, int MX>
 cudaError_t launch_mx(const RectArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
-    auto k = k_rect<MODE, MX>;
+    static const int rows_per_stage = [] {
+        const char* v = getenv("FDG_RECT_R");
+        return v ? atoi(v) : 4;
+    }();
+    auto k = rows_per_stage == 4 ? k_rect<MODE, MX, 4> : rows_per_stage == 2 ? k_rect<MODE, MX, 2> : k_rect<MODE, MX, 1>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     k<<<grid, NT + 32, smem, st>>>(a);
