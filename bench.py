@@ -132,8 +132,9 @@ def run_reference(args, cfg, world, rank):
 
 def reference_sample(cfg):
     """(rows per strip, iterations) giving ~5-10 s of single-core reference work."""
-    per_px_it_us = {"box1d-sliding": 0.011, "box2d-sliding": 0.09, "generic-box": 0.08, "naive": 1.7}[cfg.op]
-    budget = 6.0e6  # us per thread
+    # single-core reference cost per px*it measured on the B200 host (r01)
+    per_px_it_us = {"box1d-sliding": 0.011, "box2d-sliding": 0.016, "generic-box": 0.08, "naive": 1.7}[cfg.op]
+    budget = 10.0e6  # us per thread (~10 s sample)
     px_it = budget / per_px_it_us
     iters = max(2, min(cfg.iterations, 10))
     rows = int(max(16, min(cfg.height, px_it / iters / cfg.width)))

@@ -94,7 +94,6 @@ struct fdg_plan {
         cudaFree(dev.d_row_start);
         cudaFree(dev.d_dx);
         cudaFree(dev.d_w);
-        cudaFree(dev.d_span);
         cudaFree(dev.d_dense);
     }
 };
@@ -212,9 +211,24 @@ int build_plan(fdg_ctx* ctx, const HostPsf& psf, int preference, std::unique_ptr
         case FDG_OP_GENERIC_BOX: {
             psf_as_convex(psf, &pl->spans);
             int count = 0;
-            std::vector<Tap> t;
             for (const Span& s : pl->spans) count += s.xmax - s.xmin + 1;
             const double u = 1.0 / (double)count;
+            // span table (rows contiguous in dy) for the compile-time spans engine
+            d.nrows = (int)pl->spans.size();
+            d.min_dy = pl->spans.front().dy;
+            d.max_dy = pl->spans.back().dy;
+            d.h_span.clear();
+            for (const Span& s : pl->spans) {
+                d.h_span.push_back(s.xmin);
+                d.h_span.push_back(s.xmax);
+            }
+            if (spans_supported(d)) {
+                d.engine = ENG_SPANS;
+                d.uniform = 1;
+                d.scale = (float)u;
+                break;
+            }
+            std::vector<Tap> t;
             for (const Span& s : pl->spans)
                 for (int x = s.xmin; x <= s.xmax; ++x) t.push_back({x, s.dy, u});
             int st = build_taps_engine(pl.get(), t, true, u);

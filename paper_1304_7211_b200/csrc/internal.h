@@ -61,7 +61,7 @@ struct DevPsf {
     int* d_row_start = nullptr;  // [nrows+1], rows r = dy - min_dy
     int* d_dx = nullptr;         // [ntaps]
     float* d_w = nullptr;        // [ntaps]
-    int* d_span = nullptr;       // [2*nrows] xmin,xmax per row (spans engine)
+    std::vector<int> h_span;     // [2*nrows] xmin,xmax per row (spans engine, host)
     int mw = 0, mh = 0, mwp = 0;  // dense engine: grid, padded width
     float* d_dense = nullptr;     // [mh * mwp]
 };

@@ -134,3 +134,6 @@ def test_engine_selection():
     assert ConvPlan(makeBoxPsf(15, 15), K.Box2dSliding).engine() == "box"
     assert ConvPlan(W.gaussian31(), K.Naive).engine() == "dense"
     assert ConvPlan(makeDiagonalPsf(9), K.List).engine() == "taps"
+    assert ConvPlan(W.disc_r10(), K.GenericBox).engine() == "spans"
+    assert ConvPlan(W.oblique_line(), K.GenericBox).engine() == "spans"
+    assert ConvPlan(makeDiscPsf(9), K.GenericBox).engine() == "taps"
