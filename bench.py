@@ -186,14 +186,18 @@ def run_ours(args, cfg, world, rank, local):
     stream = torch.cuda.current_stream(dev)
     solver.use_stream(stream.cuda_stream)
 
-    if s is not None:
+    if s is not None and world > 1:
         passes = S.GpuPasses(solver)
 
         def step():
             S.rl_strips(f_dev, s, iters, passes, u=u_dev, q=q_dev)
     else:
+        # one process, whole image(s): the C driver loop, replayed as a CUDA graph
+        f_run = f_dev[s.halo:s.halo + s.core] if s is not None else f_dev
+        u_run = u_dev[s.halo:s.halo + s.core] if s is not None else u_dev
+
         def step():
-            solver.run(f_dev, u_dev, iters)
+            solver.run(f_run, u_run, iters)
 
     # ---- warmup
     for _ in range(args.warmup):

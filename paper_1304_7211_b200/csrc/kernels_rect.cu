@@ -251,17 +251,23 @@ __global__ void __launch_bounds__(NT + 32) k_rect(const RectArgs a) {
     if (MODE == EPI_UPDATE) trace_flush(a.e, tr);
 }
 
+template <int MODE, int MX, int R>
+cudaError_t launch_r(const RectArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
+    cudaError_t err = smem_attr<k_rect<MODE, MX, R>>();
+    if (err != cudaSuccess) return err;
+    k_rect<MODE, MX, R><<<grid, NT + 32, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
 template <int MODE, int MX>
 cudaError_t launch_mx(const RectArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
     static const int rows_per_stage = [] {
         const char* v = getenv("FDG_RECT_R");
         return v ? atoi(v) : 4;
     }();
-    auto k = rows_per_stage == 4 ? k_rect<MODE, MX, 4> : rows_per_stage == 2 ? k_rect<MODE, MX, 2> : k_rect<MODE, MX, 1>;
-    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    k<<<grid, NT + 32, smem, st>>>(a);
-    return cudaGetLastError();
+    if (rows_per_stage == 1) return launch_r<MODE, MX, 1>(a, grid, smem, st);
+    if (rows_per_stage == 2) return launch_r<MODE, MX, 2>(a, grid, smem, st);
+    return launch_r<MODE, MX, 4>(a, grid, smem, st);
 }
 
 template <int MODE, int... MXS>

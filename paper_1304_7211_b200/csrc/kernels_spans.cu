@@ -265,10 +265,9 @@ template <int MODE, class SH, int NT>
 cudaError_t launch_t(const SpanArgs& a, dim3 grid, cudaStream_t st) {
     using E = Ext<SH, NT>;
     const size_t smem = 128 + sizeof(float) * ((size_t)S * E::SEG + (size_t)S * E::CW);
-    auto k = k_spans<MODE, SH, NT>;
-    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t err = smem_attr<k_spans<MODE, SH, NT>>();
     if (err != cudaSuccess) return err;
-    k<<<grid, NT + 32, smem, st>>>(a);
+    k_spans<MODE, SH, NT><<<grid, NT + 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 

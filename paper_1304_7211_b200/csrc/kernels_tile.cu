@@ -97,10 +97,9 @@ __global__ void __launch_bounds__(256) k_taps(const TapsArgs a) {
 
 template <int MODE, bool MASKED>
 cudaError_t launch_taps_t(const TapsArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
-    auto k = k_taps<MODE, MASKED>;
-    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t err = smem_attr<k_taps<MODE, MASKED>>();
     if (err != cudaSuccess) return err;
-    k<<<grid, dim3(32, 8), smem, st>>>(a);
+    k_taps<MODE, MASKED><<<grid, dim3(32, 8), smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -205,10 +204,9 @@ __global__ void __launch_bounds__(256, 2) k_dense(const DenseArgs a) {
 
 template <int MWP, int MODE, bool MASKED>
 cudaError_t launch_dense_t(const DenseArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
-    auto k = k_dense<MWP, MODE, MASKED>;
-    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t err = smem_attr<k_dense<MWP, MODE, MASKED>>();
     if (err != cudaSuccess) return err;
-    k<<<grid, 256, smem, st>>>(a);
+    k_dense<MWP, MODE, MASKED><<<grid, 256, smem, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -177,3 +177,30 @@ def test_validation_messages():
         rlDeconvolveSelective(f, makeBoxPsf(1, 1), RlConfig(), 0.1, 0)
     with pytest.raises(ValueError, match="masked evaluation"):
         rlDeconvolveSelective(f, makeDiscPsf(3), RlConfig(op=K.GenericBox), 0.1)
+
+
+def test_device_solver_graph_replay_matches_host_api():
+    import torch
+    from paper_1304_7211_b200 import RlSolver
+    from paper_1304_7211_b200 import sharded as S
+    cfg = W.CONFIGS["cfg4"]
+    _, f = W.make_input(cfg, 768, 320)
+    psf = W.make_psf(cfg.psf)
+    rc = RlConfig(iterations=25, op=K.Box2dSliding)
+    host = rlDeconvolve(f, psf, rc).image
+    dev = torch.device("cuda", 0)
+    fd = torch.from_numpy(f).to(dev)
+    ud = torch.empty_like(fd)
+    solver = RlSolver(psf, rc, 768, 320)
+    solver.use_stream(torch.cuda.current_stream(dev).cuda_stream)
+    for _ in range(3):  # eager, capture, replay
+        solver.run(fd, ud)
+        torch.cuda.synchronize()
+        assert np.array_equal(ud.cpu().numpy(), host)
+    # the row-strip driver with a single rank (no exchange) runs the same passes
+    s = S.strip_of(320, 1, 0, 0)
+    u2 = S.rl_strips(fd.clone(), s, 25, S.GpuPasses(solver))
+    torch.cuda.synchronize()
+    assert np.array_equal(u2.cpu().numpy(), host)
+    mc = [m for m, _ in solver.trace(25)]
+    assert all(m > 0 for m in mc)
