@@ -37,7 +37,7 @@ ref: $(REFLIB)
 cpptests: $(DROPIN)
 
 $(LIB): $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC) -lcudart
+	$(NVCC) $(NVFLAGS) -Xcompiler -fopenmp -shared -o $@ $(CSRC) -lcudart -lgomp
 
 $(ORACLE): oracle/psf.c oracle/conv.c oracle/rl.c oracle/oracle.h oracle/plan.h
 	$(HOSTCC) -O3 -std=c11 -D_POSIX_C_SOURCE=200809L -fopenmp -ffp-contract=off -fPIC -shared \

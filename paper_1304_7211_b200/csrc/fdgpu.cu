@@ -13,9 +13,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -64,7 +66,9 @@ struct DevBuf {
     }
 };
 
-int pitch_for(int W) { return (W + 31) & ~31; }  // 128-byte rows
+// row pitch of library-owned planes: W itself when rows are 16-byte
+// multiples (contiguous copies, TMA-legal), else padded to 128 bytes
+int pitch_for(int W) { return (W % 4 == 0) ? W : ((W + 31) & ~31); }
 
 }  // namespace
 
@@ -73,9 +77,12 @@ struct fdg_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     uint64_t launches = 0;
-    // scratch for the host-buffer entry points
+    // scratch for the host-buffer entry points (kept across calls)
     DevBuf<float> a, b, c, d;
     DevBuf<uint8_t> m;
+    DevBuf<unsigned> tr_max;
+    DevBuf<int> tr_nan;
+    DevBuf<unsigned long long> tr_inact, first_bad;
 };
 
 struct fdg_plan {
@@ -377,14 +384,147 @@ int check_device(fdg_ctx* ctx) {
     return FDG_OK;
 }
 
+// ---- host <-> device copies.  Pinned (or registered) host memory goes
+// straight to the DMA engines.  Pageable memory is staged through two pinned
+// chunks: the DMA of one chunk overlaps a multi-threaded (OpenMP) memcpy of
+// the other, instead of the driver's single-threaded pageable path (measured
+// 4.7 GB/s for a 1 GiB D2H into a fresh numpy array on the B200 host).
+struct Staging {
+    static constexpr size_t CHUNK = 32u << 20;
+    std::mutex mu;
+    float* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaError_t init() {
+        if (buf[0]) return cudaSuccess;
+        for (int i = 0; i < 2; ++i) {
+            cudaError_t e = cudaHostAlloc(&buf[i], CHUNK, cudaHostAllocDefault);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
+};
+Staging& staging() {
+    static Staging* s = new Staging();  // process lifetime (pinned memory freed at exit)
+    return *s;
+}
+
+bool pageable(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+    const int nt = bytes >= (8u << 20) ? 16 : 1;
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (int t = 0; t < nt; ++t) {
+        const size_t a = bytes * t / nt, b = bytes * (t + 1) / nt;
+        std::memcpy((char*)dst + a, (const char*)src + a, b - a);
+    }
+}
+
+// touch every page of a large pageable host buffer (multi-threaded)
+void prefault(void* p, size_t bytes) {
+    if (bytes < (16u << 20) || !pageable(p)) return;
+    const size_t page = 4096;
+    char* c = static_cast<char*>(p);
+#pragma omp parallel for num_threads(16) schedule(static)
+    for (long long off = 0; off < (long long)bytes; off += page) c[off] = 0;
+}
+
 int h2d(float* d, int pitch, const float* h, int W, int H, cudaStream_t st) {
-    CK(cudaMemcpy2DAsync(d, (size_t)pitch * 4, h, (size_t)W * 4, (size_t)W * 4, H, cudaMemcpyHostToDevice, st));
+    const size_t row = (size_t)W * 4;
+    if (row * H < (4u << 20) || !pageable(h)) {
+        CK(cudaMemcpy2DAsync(d, (size_t)pitch * 4, h, row, row, H, cudaMemcpyHostToDevice, st));
+        return FDG_OK;
+    }
+    Staging& S = staging();
+    std::lock_guard<std::mutex> lock(S.mu);
+    CK(S.init());
+    const int rows_per = (int)std::max<size_t>(1, Staging::CHUNK / row);
+    for (int r0 = 0, k = 0; r0 < H; r0 += rows_per, k ^= 1) {
+        const int nr = std::min(rows_per, H - r0);
+        CK(cudaEventSynchronize(S.ev[k]));  // the previous DMA out of this chunk is done
+        par_memcpy(S.buf[k], h + (size_t)r0 * W, row * nr);
+        CK(cudaMemcpy2DAsync(d + (size_t)r0 * pitch, (size_t)pitch * 4, S.buf[k], row, row, nr,
+                             cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(S.ev[k], st));
+    }
     return FDG_OK;
 }
+
 int d2h(float* h, const float* d, int pitch, int W, int H, cudaStream_t st) {
-    CK(cudaMemcpy2DAsync(h, (size_t)W * 4, d, (size_t)pitch * 4, (size_t)W * 4, H, cudaMemcpyDeviceToHost, st));
+    const size_t row = (size_t)W * 4;
+    if (row * H < (4u << 20) || !pageable(h)) {
+        CK(cudaMemcpy2DAsync(h, row, d, (size_t)pitch * 4, row, H, cudaMemcpyDeviceToHost, st));
+        return FDG_OK;
+    }
+    Staging& S = staging();
+    std::lock_guard<std::mutex> lock(S.mu);
+    CK(S.init());
+    const int rows_per = (int)std::max<size_t>(1, Staging::CHUNK / row);
+    const int nchunk = (H + rows_per - 1) / rows_per;
+    auto issue = [&](int c) -> cudaError_t {
+        const int r0 = c * rows_per, nr = std::min(rows_per, H - r0);
+        cudaError_t e = cudaMemcpy2DAsync(S.buf[c & 1], row, d + (size_t)r0 * pitch, (size_t)pitch * 4, row, nr,
+                                          cudaMemcpyDeviceToHost, st);
+        return e == cudaSuccess ? cudaEventRecord(S.ev[c & 1], st) : e;
+    };
+    CK(issue(0));
+    for (int c = 0; c < nchunk; ++c) {
+        if (c + 1 < nchunk) CK(issue(c + 1));  // next DMA overlaps this chunk's host copy
+        CK(cudaEventSynchronize(S.ev[c & 1]));
+        const int r0 = c * rows_per, nr = std::min(rows_per, H - r0);
+        par_memcpy(h + (size_t)r0 * W, S.buf[c & 1], row * nr);
+    }
     return FDG_OK;
 }
+
+int validate_cfg(const float* f, int W, int H, const fdg_rl_config* cfg, const char* where) {
+    const std::string w(where);
+    if (!f || W < 1 || H < 1) return set_err(FDG_EINVAL, w + ": empty input image");
+    if (!cfg) return set_err(FDG_EINVAL, w + ": null config");
+    if (cfg->iterations < 0) return set_err(FDG_EINVAL, w + ": iterations must be >= 0");
+    if (!(cfg->epsilon_div > 0.0)) return set_err(FDG_EINVAL, w + ": epsilonDiv must be positive");
+    return FDG_OK;
+}
+
+// rl.hpp:78-83 on the device: first non-finite and first negative pixel
+// (row-major index); the reference reports whichever comes first, the
+// non-finite test first for the same pixel.
+int validate_device(fdg_ctx* ctx, const float* d_f, int W, int H, int pitch, const char* where) {
+    CK(ctx->first_bad.ensure(2));
+    CK(launch_validate(d_f, W, H, pitch, ctx->first_bad.p, ctx->stream));
+    ctx->launches += 1;
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, ctx->first_bad.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const std::string w(where);
+    if (h[0] != ~0ull && h[0] <= h[1]) return set_err(FDG_EINVAL, w + ": input image has non-finite pixels");
+    if (h[1] != ~0ull) return set_err(FDG_EINVAL, w + ": input image must be nonnegative");
+    return FDG_OK;
+}
+
+struct PhaseTimer {
+    bool on = getenv("FDG_PROFILE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    std::string log;
+    void mark(const char* what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        char buf[96];
+        std::snprintf(buf, sizeof buf, " %s=%.2fms", what, std::chrono::duration<double, std::milli>(n - t).count());
+        log += buf;
+        t = n;
+    }
+    ~PhaseTimer() {
+        if (on) std::fprintf(stderr, "[fdg profile]%s\n", log.c_str());
+    }
+};
 
 int validate_rl(const float* f, int W, int H, const fdg_rl_config* cfg, const char* where) {
     const std::string w(where);
@@ -674,51 +814,71 @@ int fdg_conv_apply_masked(fdg_plan* pl, const float* in, int W, int H, const uin
 
 int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, const float* f, int W,
                       int H, float* u_out, fdg_rl_record* trace) {
-    int st = validate_rl(f, W, H, cfg, "rlDeconvolve");
+    PhaseTimer pt;
+    int st = validate_cfg(f, W, H, cfg, "rlDeconvolve");
     if (st) return st;
+    if (!ctx) {  // no device: validate on the host so the reference's errors still surface
+        if ((st = validate_rl(f, W, H, cfg, "rlDeconvolve"))) return st;
+        return check_device(ctx);
+    }
     if ((st = check_device(ctx))) return st;
     std::unique_ptr<fdg_plan> fwd, adj;
     if ((st = make_rl_plans(ctx, desc, cfg->op, &fwd, &adj))) return st;
+    pt.mark("plans");
     const int iters = cfg->iterations;
     const int pitch = pitch_for(W);
     const size_t n = (size_t)pitch * H;
     cudaStream_t s = ctx->stream;
-    DevBuf<float> df, du, dq;
-    DevBuf<unsigned> mc;
-    DevBuf<int> nf;
-    CK(df.ensure(n));
-    CK(du.ensure(n));
-    CK(dq.ensure(n));
-    CK(mc.ensure(iters + 1));
-    CK(nf.ensure(iters + 1));
-    CK(cudaMemsetAsync(mc.p, 0, sizeof(unsigned) * (iters + 1), s));
-    CK(cudaMemsetAsync(nf.p, 0, sizeof(int) * (iters + 1), s));
-    if ((st = h2d(df.p, pitch, f, W, H, s))) return st;
-    CK(cudaMemcpyAsync(du.p, df.p, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    CK(ctx->a.ensure(n));  // f
+    CK(ctx->b.ensure(n));  // u
+    CK(ctx->c.ensure(n));  // q
+    CK(ctx->tr_max.ensure(iters + 1));
+    CK(ctx->tr_nan.ensure(iters + 1));
+    float *df = ctx->a.p, *du = ctx->b.p, *dq = ctx->c.p;
+    unsigned* mc = ctx->tr_max.p;
+    int* nf = ctx->tr_nan.p;
+    pt.mark("alloc");
+    if ((st = h2d(df, pitch, f, W, H, s))) return st;
+    if ((st = validate_device(ctx, df, W, H, pitch, "rlDeconvolve"))) return st;
+    pt.mark("h2d+validate");
+    CK(cudaMemsetAsync(mc, 0, sizeof(unsigned) * (iters + 1), s));
+    CK(cudaMemsetAsync(nf, 0, sizeof(int) * (iters + 1), s));
+    CK(cudaMemcpyAsync(du, df, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
     EventPool ev;
-    CK(ev.make(iters + 1));
-    CK(cudaEventRecord(ev.ev[0], s));
+    const bool timed = trace != nullptr;
+    if (timed) {
+        CK(ev.make(iters + 1));
+        CK(cudaEventRecord(ev.ev[0], s));
+    }
     for (int k = 0; k < iters; ++k) {
         Epi e1;
         e1.mode = EPI_QUOT;
-        e1.aux = df.p;
+        e1.aux = df;
         e1.eps = (float)cfg->epsilon_div;
-        if ((st = run_pass(fwd.get(), whole(du.p, dq.p, pitch, W, H), e1, s))) return st;
+        if ((st = run_pass(fwd.get(), whole(du, dq, pitch, W, H), e1, s))) return st;
         Epi e2;
         e2.mode = EPI_UPDATE;
-        e2.aux = du.p;
+        e2.aux = du;
         e2.clamp = cfg->clamp_nonnegative;
-        e2.maxchange = mc.p + k;
-        e2.nanflag = nf.p + k;
-        if ((st = run_pass(adj.get(), whole(dq.p, du.p, pitch, W, H), e2, s))) return st;
-        CK(cudaEventRecord(ev.ev[k + 1], s));
+        e2.maxchange = mc + k;
+        e2.nanflag = nf + k;
+        if ((st = run_pass(adj.get(), whole(dq, du, pitch, W, H), e2, s))) return st;
+        if (timed) CK(cudaEventRecord(ev.ev[k + 1], s));
     }
-    if ((st = d2h(u_out, du.p, pitch, W, H, s))) return st;
+    // While the device iterates, fault in the (pageable) output pages on the
+    // host so the final D2H does not pay first-touch page faults.
+    prefault(u_out, (size_t)W * H * sizeof(float));
+    if (pt.on) {
+        CK(cudaStreamSynchronize(s));
+        pt.mark("iterate");
+    }
+    if ((st = d2h(u_out, du, pitch, W, H, s))) return st;
     std::vector<unsigned> hmc(iters + 1);
     std::vector<int> hnf(iters + 1);
-    CK(cudaMemcpyAsync(hmc.data(), mc.p, sizeof(unsigned) * (iters + 1), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hnf.data(), nf.p, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hmc.data(), mc, sizeof(unsigned) * (iters + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hnf.data(), nf, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    pt.mark("d2h");
     for (int k = 0; k < iters; ++k) {
         if (hnf[k])
             return set_err(FDG_ENAN, "rlDeconvolve: NaN in iterate at iteration " + std::to_string(k + 1));

@@ -169,3 +169,32 @@ cudaError_t launch_quot_const(const float* f, float* q, int W, int H, int pitch,
     return cudaGetLastError();
 }
 }  // namespace fdg
+
+namespace fdg {
+namespace {
+__global__ void k_validate(const float* f, int W, int H, int pitch, unsigned long long* out) {
+    unsigned bad_nf = ~0u, bad_neg = ~0u;  // row-major indices (images < 2^32 px)
+    const long long n = (long long)W * H;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const float v = f[(i / W) * (long long)pitch + (i % W)];
+        if (!isfinite(v)) bad_nf = min(bad_nf, (unsigned)i);
+        else if (v < 0.f) bad_neg = min(bad_neg, (unsigned)i);
+    }
+    bad_nf = __reduce_min_sync(0xffffffffu, bad_nf);
+    bad_neg = __reduce_min_sync(0xffffffffu, bad_neg);
+    if ((threadIdx.x & 31) == 0) {
+        if (bad_nf != ~0u) atomicMin(&out[0], (unsigned long long)bad_nf);
+        if (bad_neg != ~0u) atomicMin(&out[1], (unsigned long long)bad_neg);
+    }
+}
+__global__ void k_fill_u64(unsigned long long* p, int n) {
+    if (threadIdx.x < n) p[threadIdx.x] = ~0ull;
+}
+}  // namespace
+
+cudaError_t launch_validate(const float* f, int W, int H, int pitch, unsigned long long* out, cudaStream_t st) {
+    k_fill_u64<<<1, 32, 0, st>>>(out, 2);
+    k_validate<<<1184, 256, 0, st>>>(f, W, H, pitch, out);
+    return cudaGetLastError();
+}
+}  // namespace fdg
