@@ -103,8 +103,8 @@ def run_reference(args, cfg, world, rank):
           "naive": O.NAIVE}[cfg.op]
     threads = os.cpu_count() or 1
     strip_rows, iters = reference_sample(cfg)
-    rows = min(cfg.height, threads * strip_rows + 64)
-    _, f = W.make_input(cfg, cfg.width, rows) if cfg.batch == 1 else W.make_input(cfg, cfg.width, rows)
+    rows = min(cfg.height, strip_rows + 64)  # threads run independent strips of this sample
+    _, f = W.make_input(cfg, cfg.width, rows)
     f64 = f.astype(np.float64)
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfdref.so not built"}))
@@ -131,14 +131,19 @@ def run_reference(args, cfg, world, rank):
 
 
 def reference_sample(cfg):
-    """(rows per strip, iterations) giving ~5-10 s of single-core reference work."""
+    """(rows per strip, iterations): ~10 s of single-core reference work per
+    thread, at the config's width, on a strip short enough that generating
+    its input takes well under a second."""
     # single-core reference cost per px*it measured on the B200 host (r01)
     per_px_it_us = {"box1d-sliding": 0.011, "box2d-sliding": 0.016, "generic-box": 0.08, "naive": 1.7}[cfg.op]
-    budget = 10.0e6  # us per thread (~10 s sample)
+    budget = 10.0e6  # us per thread
     px_it = budget / per_px_it_us
-    iters = max(2, min(cfg.iterations, 10))
-    rows = int(max(16, min(cfg.height, px_it / iters / cfg.width)))
-    return rows, iters
+    iters = cfg.iterations
+    rows = int(px_it / iters / cfg.width)
+    if rows < 32:  # expensive operators: fewer iterations instead of thinner strips
+        rows = 32
+        iters = max(2, int(px_it / rows / cfg.width))
+    return min(rows, cfg.height), min(iters, cfg.iterations)
 
 
 # ---------------------------------------------------------------- our path
@@ -351,7 +356,7 @@ def cpu_baseline(cfg):
               "naive": O.NAIVE}[cfg.op]
         threads = os.cpu_count() or 1
         strip_rows, iters = reference_sample(cfg)
-        rows = min(cfg.height, threads * strip_rows + 64)
+        rows = min(cfg.height, strip_rows + 64)
         _, f = W.make_input(cfg, cfg.width, rows)
         secs, pxit = O.ref_bench_strips(f.astype(np.float64), psf, op, iters, threads, strip_rows)
         return {"value": pxit / secs / 1e6, "unit": "Mpx*it/s", "cores": threads, "kind": "reference",

@@ -1,0 +1,105 @@
+#!/usr/bin/env python
+"""Full-size parity of the B200 path against the CPU oracle on every BASELINE
+configuration (run on the GPU box; the oracle is OpenMP-threaded and
+bit-identical to the reference).  Writes profiles/r01_full_parity.json.
+
+  python scripts/full_parity.py [cfg0 cfg1 ...]
+
+Per config: max-rel = max|u_gpu - u_ref| / |u_ref|, PSNR(u, g) for both
+(peak 1), |dPSNR|, PSNR(u_gpu vs u_ref), wall times.  cfg3 additionally runs
+the thinned variants (thinning from iteration 20, thresholds calibrated to
+~50 % / ~25 % active, profiles/r01_cfg3_thresholds.json) with the oracle's
+per-iteration masks replayed on the device: active lists / runs bit-exact,
+image within the bound.  cfg4b checks 8 of the 64 images.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import pyoracle as O  # noqa: E402
+from paper_1304_7211_b200 import OperatorKind as K, RlConfig, rlDeconvolve, rlDeconvolveSelective  # noqa: E402
+from paper_1304_7211_b200 import workloads as W  # noqa: E402
+from paper_1304_7211_b200.convolve import maskRuns  # noqa: E402
+
+OPS = {"box1d-sliding": K.Box1dSliding, "box2d-sliding": K.Box2dSliding, "generic-box": K.GenericBox,
+       "naive": K.Naive}
+
+
+def compare(name, g, f, psf, op, it, extra=None):
+    t = time.time()
+    res = rlDeconvolve(f, psf, RlConfig(iterations=it, op=op))
+    tg = time.time() - t
+    t = time.time()
+    ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, it, int(op))
+    to = time.time() - t
+    row = {"config": name, "size": list(f.shape), "iterations": it, "op": op.name,
+           "max_rel": W.max_rel(res.image, ref), "psnr_gpu": W.psnr(res.image, g), "psnr_ref": W.psnr(ref, g),
+           "psnr_gpu_vs_ref": W.psnr(res.image, ref), "gpu_s": tg, "oracle_s": to,
+           "oracle_threads": O.num_threads()}
+    row["dpsnr"] = abs(row["psnr_gpu"] - row["psnr_ref"])
+    row["pass"] = row["max_rel"] <= 1e-4 and row["dpsnr"] <= 0.01
+    if extra:
+        row.update(extra)
+    print(json.dumps(row), flush=True)
+    return row
+
+
+def thinned(name, g, f, psf, it, thr, label):
+    t = time.time()
+    ref, inact, _, masks = O.rl_selective(f.astype(np.float64), psf, it, thr, 10, 20, O.NAIVE, record_masks=True)
+    to = time.time() - t
+    t = time.time()
+    res = rlDeconvolveSelective(f, psf, RlConfig(iterations=it, op=K.Naive), thr, 10, thin_start=20,
+                                mask_replay=masks, record_masks=True)
+    tg = time.time() - t
+    masks_equal = bool(np.array_equal(res.masks, masks))
+    runs_equal = True
+    for k in (20, 21, 75, it - 1):
+        idx, runs = maskRuns(masks[k])
+        runs_equal &= bool(np.array_equal(idx, O.active_list(masks[k])) and np.array_equal(runs, O.mask_runs(masks[k])))
+    row = {"config": name, "variant": label, "threshold": thr, "size": list(f.shape), "iterations": it,
+           "active_fraction_it21_150": float(1 - inact[20:].mean()),
+           "gpu_inactive_equal": bool(np.allclose([r.inactiveFraction for r in res.trace.records], inact, atol=0)),
+           "masks_equal": masks_equal, "lists_runs_bit_exact": runs_equal,
+           "max_rel": W.max_rel(res.image, ref), "psnr_gpu": W.psnr(res.image, g), "psnr_ref": W.psnr(ref, g),
+           "gpu_s": tg, "oracle_s": to}
+    row["dpsnr"] = abs(row["psnr_gpu"] - row["psnr_ref"])
+    row["pass"] = row["max_rel"] <= 1e-4 and row["dpsnr"] <= 0.01 and masks_equal and runs_equal
+    print(json.dumps(row), flush=True)
+    return row
+
+
+def main():
+    which = sys.argv[1:] or ["cfg0", "cfg1", "cfg2", "cfg3", "cfg4", "cfg4b"]
+    rows = []
+    out = os.path.join(ROOT, "profiles", "r01_full_parity.json")
+    for name in which:
+        cfg = W.CONFIGS[name]
+        psf = W.make_psf(cfg.psf)
+        op = OPS[cfg.op]
+        if name == "cfg4b":
+            for i in range(0, 64, 8):
+                g, f = W.make_input(cfg, image=i)
+                rows.append(compare(f"{name}[{i}]", g, f, psf, op, cfg.iterations))
+            continue
+        g, f = W.make_input(cfg)
+        rows.append(compare(name, g, f, psf, op, cfg.iterations))
+        if name == "cfg3":
+            thr_path = os.path.join(ROOT, "profiles", "r01_cfg3_thresholds.json")
+            if os.path.exists(thr_path):
+                thr = json.load(open(thr_path))
+                for label in ("active50", "active25"):
+                    if label in thr:
+                        rows.append(thinned(name, g, f, psf, cfg.iterations, thr[label]["threshold"], label))
+        json.dump(rows, open(out, "w"), indent=1)
+    json.dump(rows, open(out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
