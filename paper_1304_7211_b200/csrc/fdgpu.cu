@@ -363,6 +363,24 @@ int run_pass(fdg_plan* pl, const Geom& g, const Epi& e, cudaStream_t st) {
     return FDG_OK;
 }
 
+// Row-resident RL (kernels_rowres.cu) serves horizontal lines at dy = 0:
+// every row evolves independently, so all iterations run in shared memory.
+bool use_rowres(const fdg_plan* pl, int W) {
+    static const bool off = getenv("FDG_NO_ROWRES") != nullptr;
+    const DevPsf& d = pl->dev;
+    return !off && d.engine == ENG_RECT && rowres_supported(d.mx, d.my, d.min_dy, W);
+}
+
+int run_rowres(fdg_plan* pl, const float* f, float* u, int pitch, int W, int H, int batch, long long bstride,
+               int iters, const fdg_rl_config* cfg, unsigned* mc, int* nf, cudaStream_t st) {
+    const DevPsf& d = pl->dev;
+    cudaError_t r = launch_rowres(d.mx, d.min_dx, d.scale, f, u, pitch, W, H, batch, bstride, iters,
+                                  (float)cfg->epsilon_div, cfg->clamp_nonnegative, mc, nf, st);
+    if (r != cudaSuccess) return cuda_err(r, "row-resident RL launch");
+    pl->ctx->launches += 1;
+    return FDG_OK;
+}
+
 Geom whole(const float* in, float* out, int pitch, int W, int H, int batch = 1, long long bstride = 0) {
     Geom g;
     g.in = in;
@@ -846,11 +864,16 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     CK(cudaMemcpyAsync(du, df, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
     EventPool ev;
     const bool timed = trace != nullptr;
+    const bool rowres = use_rowres(fwd.get(), W) && iters > 0;
     if (timed) {
         CK(ev.make(iters + 1));
         CK(cudaEventRecord(ev.ev[0], s));
     }
-    for (int k = 0; k < iters; ++k) {
+    if (rowres) {  // all iterations in one launch; per-iteration seconds = run time / iterations
+        if ((st = run_rowres(fwd.get(), df, du, pitch, W, H, 1, 0, iters, cfg, mc, nf, s))) return st;
+        if (timed) CK(cudaEventRecord(ev.ev[iters], s));
+    }
+    for (int k = 0; k < (rowres ? 0 : iters); ++k) {
         Epi e1;
         e1.mode = EPI_QUOT;
         e1.aux = df;
@@ -884,7 +907,10 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
             return set_err(FDG_ENAN, "rlDeconvolve: NaN in iterate at iteration " + std::to_string(k + 1));
         if (trace) {
             float ms = 0.f;
-            cudaEventElapsedTime(&ms, ev.ev[k], ev.ev[k + 1]);
+            if (rowres)
+                cudaEventElapsedTime(&ms, ev.ev[0], ev.ev[iters]), ms /= (float)iters;
+            else
+                cudaEventElapsedTime(&ms, ev.ev[k], ev.ev[k + 1]);
             float m;
             std::memcpy(&m, &hmc[k], sizeof m);
             trace[k] = {k + 1, 0.0, (double)m, ms * 1e-3};
@@ -1154,7 +1180,11 @@ int fdg_solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long 
         return FDG_OK;
     }
     const uint64_t before = s->ctx->launches;
+    const bool rowres = use_rowres(s->fwd.get(), s->W) && iterations > 0 && iterations <= s->ntrace;
     auto issue = [&]() -> int {
+        if (rowres)
+            return run_rowres(s->fwd.get(), d_f, d_u, pitch, s->W, s->H, s->batch, stride, iterations, &s->cfg,
+                              s->maxchange.p, s->nanflag.p, s->ctx->stream);
         CK(cudaMemcpyAsync(d_u, d_f, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
         for (int k = 0; k < iterations; ++k) {
             int r = fdg_solver_pass(s, 1, d_u, d_f, s->q.p, pitch, stride, 0, s->H, 0, s->H - 1, k);

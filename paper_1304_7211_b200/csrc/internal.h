@@ -124,6 +124,10 @@ cudaError_t launch_row_runs_emit(const uint8_t* active, int W, int H, const long
 cudaError_t launch_quot_const(const float* f, float* q, int W, int H, int pitch, long long bstride, int batch,
                               float c, float eps, cudaStream_t st);
 bool rect_supported(int mx);
+bool rowres_supported(int mx, int my, int min_dy, int W);
+cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float* u, int pitch, int W, int H,
+                          int batch, long long bstride, int iters, float eps, int clamp, unsigned* maxchange,
+                          int* nanflag, cudaStream_t st);
 // first non-finite / first negative row-major index (~0 if none) -> out[0..1]
 cudaError_t launch_validate(const float* f, int W, int H, int pitch, unsigned long long* out, cudaStream_t st);
 cudaError_t launch_count_inactive(const uint8_t* active, size_t n, unsigned long long* out,
