@@ -368,7 +368,7 @@ int run_pass(fdg_plan* pl, const Geom& g, const Epi& e, cudaStream_t st) {
 bool use_rowres(const fdg_plan* pl, int W) {
     static const bool off = getenv("FDG_NO_ROWRES") != nullptr;
     const DevPsf& d = pl->dev;
-    return !off && d.engine == ENG_RECT && rowres_supported(d.mx, d.my, d.min_dy, W);
+    return !off && d.engine == ENG_RECT && rowres_supported(d.mx, d.my, d.min_dx, d.min_dy, W);
 }
 
 int run_rowres(fdg_plan* pl, const float* f, float* u, int pitch, int W, int H, int batch, long long bstride,

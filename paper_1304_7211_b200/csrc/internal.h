@@ -124,7 +124,7 @@ cudaError_t launch_row_runs_emit(const uint8_t* active, int W, int H, const long
 cudaError_t launch_quot_const(const float* f, float* q, int W, int H, int pitch, long long bstride, int batch,
                               float c, float eps, cudaStream_t st);
 bool rect_supported(int mx);
-bool rowres_supported(int mx, int my, int min_dy, int W);
+bool rowres_supported(int mx, int my, int min_dx, int min_dy, int W);
 cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float* u, int pitch, int W, int H,
                           int batch, long long bstride, int iters, float eps, int clamp, unsigned* maxchange,
                           int* nanflag, cudaStream_t st);

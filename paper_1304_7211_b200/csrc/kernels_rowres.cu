@@ -36,30 +36,64 @@ struct RowResArgs {
     int* nanflag;         // [iters]
 };
 
-template <int M>
-__device__ __forceinline__ void window_sums(const float* row, int W, int xb, int off, float (&out)[PT]) {
-    // out[i] = sum_{k<M} row[clamp(xb + i + off + k)]
-    constexpr int NW = PT + M - 1;
-    float w[NW];
-    const int lo = xb + off;
-    if (lo >= 0 && lo + NW - 1 <= W - 1) {
-#pragma unroll
-        for (int k = 0; k < NW; ++k) w[k] = row[lo + k];
+template <int N>
+__device__ __forceinline__ float tsum(const float* v) {
+    if constexpr (N == 1) {
+        return v[0];
     } else {
-#pragma unroll
-        for (int k = 0; k < NW; ++k) w[k] = row[clampi(lo + k, 0, W - 1)];
+        return tsum<N / 2>(v) + tsum<N - N / 2>(v + N / 2);
     }
-    float p[NW];
-    p[0] = w[0];
-#pragma unroll
-    for (int k = 1; k < NW; ++k) p[k] = p[k - 1] + w[k];
-    out[0] = p[M - 1];
-#pragma unroll
-    for (int i = 1; i < PT; ++i) out[i] = p[i + M - 1] - p[i - 1];
 }
 
-template <int M>
-__global__ void __launch_bounds__(256) k_rowres(const RowResArgs a) {
+// out[i] = sum_{k<M} row[clamp(xb + i + off + k)], i < PT (M >= PT).
+// Interior threads read aligned float4 chunks (the window start sits at
+// OFF4 = off & 3 inside its chunk, xb being a multiple of 8); threads at the
+// row ends read clamped scalars.  Sums are formed without subtraction:
+// shared middle (balanced tree) + left suffix + right prefix, dependency
+// depth ~log2(M) + PT instead of a length-M chain.
+template <int M, int OFF4>
+__device__ __forceinline__ void window_sums(const float* row, int W, int xb, int off, float (&out)[PT]) {
+    constexpr int NW = PT + M - 1;
+    constexpr int NCH = (OFF4 + NW - 1) / 4 + 1;
+    float v[4 * NCH];
+    const int lo = xb + off;
+    const int c0 = lo - OFF4;  // multiple of 4
+    if (c0 >= 0 && c0 + 4 * NCH <= W) {
+        const float4* p = reinterpret_cast<const float4*>(row + c0);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const float4 q = p[c];
+            v[4 * c] = q.x;
+            v[4 * c + 1] = q.y;
+            v[4 * c + 2] = q.z;
+            v[4 * c + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < NW; ++k) v[OFF4 + k] = row[clampi(lo + k, 0, W - 1)];
+    }
+    const float* w = v + OFF4;
+    const float mid = tsum<M - PT + 1>(w + PT - 1);  // taps common to all PT windows
+    float left = 0.f, right = 0.f;
+    float L[PT], Rr[PT];
+#pragma unroll
+    for (int i = PT - 2; i >= 0; --i) {  // L[i] = sum_{k=i}^{PT-2} w[k]
+        left += w[i];
+        L[i] = left;
+    }
+    L[PT - 1] = 0.f;
+    Rr[0] = 0.f;
+#pragma unroll
+    for (int i = 1; i < PT; ++i) {  // Rr[i] = sum_{k=M}^{M+i-1} w[k]
+        right += w[M + i - 1];
+        Rr[i] = right;
+    }
+#pragma unroll
+    for (int i = 0; i < PT; ++i) out[i] = (L[i] + mid) + Rr[i];
+}
+
+template <int M, int O1, int O2>
+__global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
     extern __shared__ __align__(16) float sm[];
     const int W = a.W;
     const int wp = (W + 3) & ~3;
@@ -102,34 +136,68 @@ __global__ void __launch_bounds__(256) k_rowres(const RowResArgs a) {
     const int off1 = a.min_dx;               // forward window start
     const int off2 = -(a.min_dx + M - 1);    // adjoint window start (offsets negated)
     for (int it = 0; it < a.iters; ++it) {
+        // own 8 columns move as two float4 (scalar smem accesses at an
+        // 8-float lane stride would conflict 8-way)
+        const bool vec = xb + PT <= W;
         if (active) {
             float v[PT];
-            window_sums<M>(ru, W, xb, off1, v);
+            window_sums<M, O1>(ru, W, xb, off1, v);
+            float fv[PT], qv[PT];
+            if (vec) {
+                const float4 a0 = *reinterpret_cast<const float4*>(rf + xb);
+                const float4 a1 = *reinterpret_cast<const float4*>(rf + xb + 4);
+                fv[0] = a0.x, fv[1] = a0.y, fv[2] = a0.z, fv[3] = a0.w;
+                fv[4] = a1.x, fv[5] = a1.y, fv[6] = a1.z, fv[7] = a1.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < PT; ++i) fv[i] = xb + i < W ? rf[xb + i] : 1.f;
+            }
 #pragma unroll
             for (int i = 0; i < PT; ++i) {
-                const int x = xb + i;
-                if (x < W) {
-                    const float d = v[i] * a.inv_m;
-                    rq[x] = div_fast(rf[x], d < a.eps ? a.eps : d);
-                }
+                const float d = v[i] * a.inv_m;
+                qv[i] = div_fast(fv[i], d < a.eps ? a.eps : d);
+            }
+            if (vec) {
+                *reinterpret_cast<float4*>(rq + xb) = make_float4(qv[0], qv[1], qv[2], qv[3]);
+                *reinterpret_cast<float4*>(rq + xb + 4) = make_float4(qv[4], qv[5], qv[6], qv[7]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < PT; ++i)
+                    if (xb + i < W) rq[xb + i] = qv[i];
             }
         }
         __syncthreads();
         float maxd = 0.f, csum = 0.f;
         if (active) {
             float c[PT];
-            window_sums<M>(rq, W, xb, off2, c);
+            window_sums<M, O2>(rq, W, xb, off2, c);
+            float uv[PT];
+            if (vec) {
+                const float4 a0 = *reinterpret_cast<const float4*>(ru + xb);
+                const float4 a1 = *reinterpret_cast<const float4*>(ru + xb + 4);
+                uv[0] = a0.x, uv[1] = a0.y, uv[2] = a0.z, uv[3] = a0.w;
+                uv[4] = a1.x, uv[5] = a1.y, uv[6] = a1.z, uv[7] = a1.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < PT; ++i) uv[i] = xb + i < W ? ru[xb + i] : 0.f;
+            }
 #pragma unroll
             for (int i = 0; i < PT; ++i) {
-                const int x = xb + i;
-                if (x < W) {
-                    const float u = ru[x];
-                    float value = c[i] * a.inv_m * u;
-                    if (a.clamp && value < 0.f) value = 0.f;
-                    maxd = fmaxf(maxd, fabsf(value - u));
+                float value = c[i] * a.inv_m * uv[i];
+                if (a.clamp && value < 0.f) value = 0.f;
+                if (xb + i < W) {
+                    maxd = fmaxf(maxd, fabsf(value - uv[i]));
                     csum += value;
-                    ru[x] = value;
                 }
+                uv[i] = value;
+            }
+            if (vec) {
+                *reinterpret_cast<float4*>(ru + xb) = make_float4(uv[0], uv[1], uv[2], uv[3]);
+                *reinterpret_cast<float4*>(ru + xb + 4) = make_float4(uv[4], uv[5], uv[6], uv[7]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < PT; ++i)
+                    if (xb + i < W) ru[xb + i] = uv[i];
             }
         }
         const unsigned bits = __reduce_max_sync(0xffffffffu, __float_as_uint(maxd));
@@ -154,18 +222,25 @@ __global__ void __launch_bounds__(256) k_rowres(const RowResArgs a) {
     }
 }
 
+// anchor-centred lines (makeLinePsf): forward window starts at -(M/2), the
+// adjoint's at -(M - 1 - M/2)
+constexpr int o1_of(int m) { return (-(m / 2)) & 3; }
+constexpr int o2_of(int m) { return (-(m - 1 - m / 2)) & 3; }
+
 template <int M>
 cudaError_t launch_m(const RowResArgs& a, int threads, size_t smem, int blocks, cudaStream_t st) {
-    cudaError_t err = smem_attr<k_rowres<M>>();
+    constexpr int O1 = o1_of(M), O2 = o2_of(M);
+    cudaError_t err = smem_attr<k_rowres<M, O1, O2>>();
     if (err != cudaSuccess) return err;
-    k_rowres<M><<<blocks, threads, smem, st>>>(a);
+    k_rowres<M, O1, O2><<<blocks, threads, smem, st>>>(a);
     return cudaGetLastError();
 }
 
 }  // namespace
 
-bool rowres_supported(int mx, int my, int min_dy, int W) {
-    return my == 1 && min_dy == 0 && (mx == 15 || mx == 31 || mx == 9 || mx == 17) && W >= 1 && W <= 8192;
+bool rowres_supported(int mx, int my, int min_dx, int min_dy, int W) {
+    return my == 1 && min_dy == 0 && min_dx == -(mx / 2) && (mx == 15 || mx == 31 || mx == 9 || mx == 17) &&
+           W >= 1 && W <= 8192;
 }
 
 cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float* u, int pitch, int W, int H,
