@@ -172,16 +172,18 @@ def run_ours(args, cfg, world, rank, local):
     if cfg.batch == 1:
         halo = S.psf_halo(psf) if world > 1 else 0
         s = S.strip_of(H_, world, rank, halo)
-        f_host = make_input_gpu(cfg, psf, dev)
-        f_dev = S.load_strip(f_host, s, pitch, device=dev)
+        f_full = make_input_gpu(cfg, psf, dev)
+        f_dev = torch.zeros((s.rows, pitch), dtype=torch.float32, device=dev)
+        f_dev[s.halo:s.halo + s.core, :W_] = f_full[s.r0:s.r0 + s.core]
+        f_host = f_full.cpu().numpy() if world == 1 else None
+        del f_full
         nimg = 1
         px_local = W_ * s.core
     else:
         share = S.batch_share(cfg.batch, world, rank)
         nimg = len(share)
-        imgs = [make_input_gpu(cfg, psf, dev, image=i) for i in share]
-        f_host = np.stack(imgs)
-        f_dev = torch.from_numpy(f_host).to(dev)
+        f_dev = torch.stack([make_input_gpu(cfg, psf, dev, image=i) for i in share])
+        f_host = f_dev.cpu().numpy() if world == 1 else None
         s = None
         px_local = W_ * H_ * nimg
     setup_s = time.time() - t0
@@ -313,28 +315,32 @@ def run_ours(args, cfg, world, rank, local):
 
 
 def make_input_gpu(cfg, psf, dev, image=0):
-    """The workloads.make_input observation with the replicate blur evaluated
-    on the device (fp32, Auto operator) -- same scene and noise draws; the
-    float64 CPU blur of a 16384^2 image takes ~30 s."""
+    """The workloads.make_input observation built on the device: the seeded
+    scene is painted on the host, the replicate blur runs on the device (fp32,
+    Auto operator) and the N(0, sigma^2) noise comes from a seeded torch
+    generator on the device (the float64 CPU path takes ~45 s and ~10 GB of
+    host memory at 16384^2; every rank builds the same image).  Returns the
+    observation as a (H, W) float32 CUDA tensor."""
     import torch
     from paper_1304_7211_b200 import ConvPlan, workloads as W
+    from paper_1304_7211_b200._lib import Context
     seed = cfg.seed + image
     rng = np.random.Generator(np.random.PCG64(seed))
     g = W.scene(cfg.width, cfg.height, seed, cfg.n_rect, cfg.n_disk, rng)
     gd = torch.from_numpy(g.astype(np.float32)).to(dev)
     del g
     bd = torch.empty_like(gd)
-    plan = ConvPlan(psf)
-    plan._ctx = None
-    from paper_1304_7211_b200._lib import Context
     ctx = Context(dev.index)
     ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
-    plan._ctx = ctx
+    plan = ConvPlan(psf, ctx=ctx)
     plan.apply_device(gd.data_ptr(), bd.data_ptr(), cfg.width, cfg.height, cfg.width)
-    noise = torch.from_numpy(rng.normal(0.0, cfg.sigma, size=(cfg.height, cfg.width)).astype(np.float32)).to(dev)
+    del gd
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    noise = torch.randn(bd.shape, generator=gen, device=dev, dtype=torch.float32) * cfg.sigma
     f = torch.clamp_min(bd + noise, 1e-6)
     torch.cuda.synchronize(dev)
-    return f.cpu().numpy()
+    return f
 
 
 def solver_engine(psf, op):
