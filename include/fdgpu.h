@@ -92,6 +92,11 @@ int fdg_abi_version(void);
 const char* fdg_last_error(void);
 /* 1 when a CUDA device is usable, else 0 */
 int fdg_device_available(void);
+/* Process-wide engine options (no reference counterpart; tuning/testing):
+ *   "fused": 1 = run each RL iteration of the centred 15x15 box as one fused
+ *            pass (kernels_fused.cu), 0 = two fused-epilogue passes (default).
+ * Returns the previous value, or -1 for an unknown name. */
+int fdg_set_option(const char* name, int value);
 
 /* Context: device, stream (default: a private non-blocking stream). */
 int fdg_ctx_create(int device, fdg_ctx** out);

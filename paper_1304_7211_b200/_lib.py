@@ -93,6 +93,7 @@ def lib():
             "fdg_abi_version": (C.c_int, []),
             "fdg_last_error": (C.c_char_p, []),
             "fdg_device_available": (C.c_int, []),
+            "fdg_set_option": (C.c_int, [C.c_char_p, C.c_int]),
             "fdg_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
             "fdg_ctx_destroy": (None, [vp]),
             "fdg_ctx_set_stream": (C.c_int, [vp, vp]),

@@ -381,6 +381,22 @@ int run_rowres(fdg_plan* pl, const float* f, float* u, int pitch, int W, int H, 
     return FDG_OK;
 }
 
+// Single-pass RL iteration (kernels_fused.cu) for the centred 15x15 box: the
+// forward and adjoint passes, quotient and update in one launch.
+bool use_fused(const fdg_plan* pl) {
+    const DevPsf& d = pl->dev;
+    return d.engine == ENG_RECT && fused_supported(d.mx, d.my, d.min_dx, d.min_dy);
+}
+
+int run_fused(fdg_plan* pl, const float* u_in, const float* f, float* u_out, int pitch, int W, int H, int batch,
+              long long bstride, const fdg_rl_config* cfg, unsigned* mc, int* nf, cudaStream_t st) {
+    cudaError_t r = launch_fused(u_in, f, u_out, pitch, W, H, batch, bstride, pl->dev.scale,
+                                 (float)cfg->epsilon_div, cfg->clamp_nonnegative, mc, nf, st);
+    if (r != cudaSuccess) return cuda_err(r, "fused RL iteration launch");
+    pl->ctx->launches += 1;
+    return FDG_OK;
+}
+
 Geom whole(const float* in, float* out, int pitch, int W, int H, int batch = 1, long long bstride = 0) {
     Geom g;
     g.in = in;
@@ -591,6 +607,14 @@ extern "C" {
 
 int fdg_abi_version(void) { return FDG_ABI_VERSION; }
 const char* fdg_last_error(void) { return g_err.c_str(); }
+int fdg_set_option(const char* name, int value) {
+    if (name && std::strcmp(name, "fused") == 0) {
+        const int prev = fused_mode();
+        set_fused_mode(value);
+        return prev;
+    }
+    return -1;
+}
 
 int fdg_device_available(void) {
     int n = 0;
@@ -873,7 +897,16 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
         if ((st = run_rowres(fwd.get(), df, du, pitch, W, H, 1, 0, iters, cfg, mc, nf, s))) return st;
         if (timed) CK(cudaEventRecord(ev.ev[iters], s));
     }
-    for (int k = 0; k < (rowres ? 0 : iters); ++k) {
+    const bool fused = !rowres && use_fused(fwd.get());
+    for (int k = 0; fused && k < iters; ++k) {
+        // ping-pong so the result lands in du: iteration k writes du when
+        // (iters - 1 - k) is even; iteration 0 reads f itself (u0 = f)
+        float* dst = ((iters - 1 - k) & 1) ? dq : du;
+        const float* src = k == 0 ? df : (dst == du ? dq : du);
+        if ((st = run_fused(fwd.get(), src, df, dst, pitch, W, H, 1, 0, cfg, mc + k, nf + k, s))) return st;
+        if (timed) CK(cudaEventRecord(ev.ev[k + 1], s));
+    }
+    for (int k = 0; k < (rowres || fused ? 0 : iters); ++k) {
         Epi e1;
         e1.mode = EPI_QUOT;
         e1.aux = df;
@@ -1181,10 +1214,24 @@ int fdg_solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long 
     }
     const uint64_t before = s->ctx->launches;
     const bool rowres = use_rowres(s->fwd.get(), s->W) && iterations > 0 && iterations <= s->ntrace;
+    const bool fused = !rowres && use_fused(s->fwd.get());
     auto issue = [&]() -> int {
         if (rowres)
             return run_rowres(s->fwd.get(), d_f, d_u, pitch, s->W, s->H, s->batch, stride, iterations, &s->cfg,
                               s->maxchange.p, s->nanflag.p, s->ctx->stream);
+        if (fused) {
+            for (int k = 0; k < iterations; ++k) {
+                float* dst = ((iterations - 1 - k) & 1) ? s->q.p : d_u;
+                const float* src = k == 0 ? d_f : (dst == d_u ? s->q.p : d_u);
+                const int slot = std::min(k, s->ntrace - 1);
+                int r = run_fused(s->fwd.get(), src, d_f, dst, pitch, s->W, s->H, s->batch, stride, &s->cfg,
+                                  s->maxchange.p + slot, s->nanflag.p + slot, s->ctx->stream);
+                if (r) return r;
+            }
+            if (iterations == 0)
+                CK(cudaMemcpyAsync(d_u, d_f, n * sizeof(float), cudaMemcpyDeviceToDevice, s->ctx->stream));
+            return FDG_OK;
+        }
         CK(cudaMemcpyAsync(d_u, d_f, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
         for (int k = 0; k < iterations; ++k) {
             int r = fdg_solver_pass(s, 1, d_u, d_f, s->q.p, pitch, stride, 0, s->H, 0, s->H - 1, k);

@@ -1,0 +1,9 @@
+#!/bin/bash
+# fused-engine parity + variant sweep on the GPU box
+set -x
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_fused.py tests/test_gpu_rl.py -x -q 2>&1 | tail -25 > gpurun_out/fused_tests.log
+for v in 0 1 2 3; do
+  FDG_FUSED_V=$v timeout 300 python bench.py --steps 5 --warmup 3 > gpurun_out/fused_v$v.json 2> gpurun_out/fused_v$v.err
+done
+FDG_NO_FUSED=1 timeout 300 python bench.py --steps 5 --warmup 3 > gpurun_out/fused_off.json 2> gpurun_out/fused_off.err

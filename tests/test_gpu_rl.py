@@ -197,10 +197,11 @@ def test_device_solver_graph_replay_matches_host_api():
         solver.run(fd, ud)
         torch.cuda.synchronize()
         assert np.array_equal(ud.cpu().numpy(), host)
-    # the row-strip driver with a single rank (no exchange) runs the same passes
+    # the row-strip driver with a single rank (no exchange) runs the two-pass
+    # engine (the solver's run() fuses each iteration into one pass)
     s = S.strip_of(320, 1, 0, 0)
     u2 = S.rl_strips(fd.clone(), s, 25, S.GpuPasses(solver))
     torch.cuda.synchronize()
-    assert np.array_equal(u2.cpu().numpy(), host)
+    assert W.max_rel(u2.cpu().numpy(), host) <= 1e-5
     mc = [m for m, _ in solver.trace(25)]
     assert all(m > 0 for m in mc)
