@@ -8,24 +8,29 @@
 // 12 B/px instead of 24 B/px for the two-pass engines.  u ping-pongs between
 // two planes (neighbouring bands read u_in halos while others write u_out).
 //
-// A CTA owns CW output columns of a row band and marches down u rows
-// j = qr_lo - RY ... yb1 - 1 + 2 RY (qr_lo..qr_hi = the q rows the band needs,
-// clamped to the readable rows).  A producer warp streams, per step, the
-// replicate-clamped u row j (CW + 4 HX columns), the f row j - RY and the u
-// row j - 2 RY of the output (TMA bulk copies, R rows per mbarrier stage).
-// Consumers (4 columns / thread):
-//   A  H1 = horizontal box sum of u row j over the q columns (CW + 2 HX);
-//      vertical running sum over the last MY H1 rows (smem ring) -> v row
-//      j - RY -> q = f / max(v / (MX MY), eps), clamped to the image columns,
-//      into a double-buffered shared q row;              named barrier
-//   B  H2 = horizontal box sum of the q row over the output columns; pushed
-//      (once, or RY+1 times at the top image edge, or repeated at the bottom
-//      edge -- replicate clamping of q) into a vertical ring -> c row ->
-//      u_out = max(c / (MX MY) * u, 0) with max|du| and the NaN checksum.
-// Window sums are formed by additions only; vertical running sums are
-// rebuilt from their rings every 32 rows (fp32 drift, SURVEY 7 part 1).
+// A CTA owns CW = 4 NT - 16 output columns of a row band and marches down u
+// rows j = qr_lo - RY ... yb1 - 1 + 2 RY (qr_lo..qr_hi = the q rows the band
+// needs, clamped to the image).  A producer warp streams the replicate-clamped
+// u rows (CW + 32 columns) into a shared ring with TMA bulk copies (R rows per
+// mbarrier stage) and prefetches the matching f rows into L2.  NT consumer
+// threads, 4 columns each, run two independent stages per row step i:
+//   A(i)    H1 = horizontal box sum of u row j over the CW + 16 q columns;
+//           vertical running sum over the last MY H1 rows (shared ring) ->
+//           v row j - RY -> q = f / max(v / (MX MY), eps) (columns clamped to
+//           the image) into a double-buffered shared q row;
+//   B(i-1)  H2 = horizontal box sum of the previous q row over the output
+//           columns; pushed into a vertical ring (RY + 1 times for the first
+//           image row, repeated below the last -- replicate clamping of q) ->
+//           c row -> u_out = max(c / (MX MY) * u, 0), max|du| and NaN.
+// A(i) and B(i-1) are independent, so one named barrier per step separates
+// the q-row producer from its consumer and the two chains overlap.  f and the
+// update's u operand are loaded into registers ahead of use (both L2 hits:
+// f prefetched by the producer, u streamed 14 rows earlier).  Window sums are
+// formed by additions only; vertical running sums are rebuilt from their
+// rings every 32 rows (fp32 drift, SURVEY 7 part 1).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -33,18 +38,21 @@ namespace fdg {
 namespace {
 
 constexpr int REFRESH = 32;
+#ifndef FDG_QSLEEP
+#define FDG_QSLEEP 40
+#endif
 
 template <int RX, int RY, int NT>
 struct FG {
     static constexpr int MX = 2 * RX + 1, MY = 2 * RY + 1;
-    static constexpr int CW = 4 * NT;           // output columns
-    static constexpr int HX = (RX + 3) / 4 * 4; // aligned horizontal halo
-    static constexpr int QW = CW + 2 * HX;      // q columns
-    static constexpr int UW = CW + 4 * HX;      // u columns of a streamed row
-    static constexpr int NQT = QW / 4;          // stage-A threads
-    static constexpr int NCT = ((NQT + 31) / 32) * 32;  // consumer threads
-    static constexpr int USEG = UW + 8, QSEG = QW + 8;
-    static constexpr int OFF = HX - RX;         // window start inside its chunk
+    static constexpr int QW = 4 * NT;       // q columns (stage A)
+    static constexpr int HX = 8;            // q halo each side (>= RX, multiple of 4)
+    static constexpr int CW = QW - 2 * HX;  // output columns (stage B)
+    static constexpr int NB = CW / 4;       // stage-B threads
+    static constexpr int UW = QW + 2 * HX;  // u columns of a streamed row
+    static constexpr int USEG = UW + 8, QSEG = QW + 16;  // B reads 4 NT + 16 q columns
+    static constexpr int OFF = HX - RX;  // window start inside its chunk
+    static_assert(RX <= HX && RY <= 8, "box radius");
 };
 
 struct FusedArgs {
@@ -74,59 +82,100 @@ __device__ __forceinline__ float4 hsum_fast(const float* seg, int chunk) {
         v[4 * c + 2] = q.z;
         v[4 * c + 3] = q.w;
     }
-    float mid = 0.f;
-#pragma unroll
-    for (int k = 3; k < MX; ++k) mid += v[OFF + k];
+    static_assert(MX == 15, "tree below is written for 15-wide windows");
+    // shared middle v[OFF+3 .. OFF+14] as a balanced tree (short dependency chain)
+    const float m01 = (v[OFF + 3] + v[OFF + 4]) + (v[OFF + 5] + v[OFF + 6]);
+    const float m23 = (v[OFF + 7] + v[OFF + 8]) + (v[OFF + 9] + v[OFF + 10]);
+    const float m45 = (v[OFF + 11] + v[OFF + 12]) + (v[OFF + 13] + v[OFF + 14]);
+    const float mid = (m01 + m23) + m45;
     const float l2 = v[OFF + 2], l1 = v[OFF + 1] + l2, l0 = v[OFF] + l1;
     const float r1 = v[OFF + MX], r2 = r1 + v[OFF + MX + 1], r3 = r2 + v[OFF + MX + 2];
     return make_float4(l0 + mid, (l1 + mid) + r1, (l2 + mid) + r2, mid + r3);
 }
 
-// clamped variant: column c of the window sum uses image columns
-// clamp(cc, 0, W-1) where cc = clamp(c, 0, W-1) + dx  (q columns outside the
-// image are replaced by the clamped column's value -- replicate semantics)
-template <int MX>
-__device__ __forceinline__ float4 hsum_clamped(const float* seg, int seg_col0, int c0, int rx, int W, bool clamp_out) {
-    float h[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int c = clamp_out ? clampi(c0 + j, 0, W - 1) : c0 + j;
-        float s = 0.f;
-        for (int k = 0; k < MX; ++k) s += seg[clampi(c - rx + k, 0, W - 1) - seg_col0];
-        h[j] = s;
+// component k (0..3) of v, for the q columns outside the image that take the
+// clamped column's value
+__device__ __forceinline__ float pick(const float4 v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
+__device__ __forceinline__ float4 pick4(const float4 v, const int4 k) {
+    return make_float4(pick(v, k.x), pick(v, k.y), pick(v, k.z), pick(v, k.w));
+}
+
+// max that propagates NaN (the reference's clamp `value < 0 ? 0 : value`
+// keeps a NaN, and a NaN anywhere must reach the per-iteration check)
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+// vertical running sum over a ring of MY rows of float4 (one slot per thread)
+template <int MY>
+struct VRing {
+    float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
+    int n = 0, slot = 0;
+    // steady state: the ring is full
+    __device__ __forceinline__ void push_full(float4* ring, int stride, int t, const float4 h) {
+        float4* rs = ring + (size_t)slot * stride + t;
+        const float4 o = *rs;
+        col.x = (col.x - o.x) + h.x;
+        col.y = (col.y - o.y) + h.y;
+        col.z = (col.z - o.z) + h.z;
+        col.w = (col.w - o.w) + h.w;
+        *rs = h;
+        slot = slot + 1 == MY ? 0 : slot + 1;
     }
-    return make_float4(h[0], h[1], h[2], h[3]);
-}
-
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-__device__ __forceinline__ void add4(float4& a, const float4& b) {
-    a.x += b.x;
-    a.y += b.y;
-    a.z += b.z;
-    a.w += b.w;
-}
-__device__ __forceinline__ void sub4(float4& a, const float4& b) {
-    a.x -= b.x;
-    a.y -= b.y;
-    a.z -= b.z;
-    a.w -= b.w;
-}
+    __device__ __forceinline__ void refresh(const float4* ring, int stride, int t) {
+        float4 fr = ring[t];
+#pragma unroll
+        for (int k = 1; k < MY; ++k) {
+            const float4 o = ring[(size_t)k * stride + t];
+            fr.x += o.x;
+            fr.y += o.y;
+            fr.z += o.z;
+            fr.w += o.w;
+        }
+        col = fr;
+    }
+    __device__ __forceinline__ void push(float4* ring, int stride, int t, const float4 h) {
+        if (n >= MY) {
+            push_full(ring, stride, t, h);
+        } else {
+            col.x += h.x;
+            col.y += h.y;
+            col.z += h.z;
+            col.w += h.w;
+            ring[(size_t)slot * stride + t] = h;
+            slot = slot + 1 == MY ? 0 : slot + 1;
+        }
+        ++n;
+        if (n > MY && (n & (REFRESH - 1)) == 0) refresh(ring, stride, t);  // fp32 drift
+    }
+};
 
 template <int RX, int RY, int NT, int R, int S>
-__global__ void __launch_bounds__(FG<RX, RY, NT>::NCT + 32) k_fused(const FusedArgs a) {
+__global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     using G = FG<RX, RY, NT>;
+    static_assert(R == 2, "stage logic assumes two rows per stage");
     constexpr int SS = S / R;
+    constexpr int LAG = SS / 2;  // edge CTAs: the producer readies stage st - LAG
     constexpr int MY = G::MY;
+    constexpr int QR = 8;        // q ring rows between the A and B warps
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     uint64_t* empty = full + SS;
-    float* uring = reinterpret_cast<float*>(smem_raw + 256);
-    float* fring = uring + S * G::USEG;
-    float* aring = fring + S * G::QSEG;
-    float* qbuf = aring + S * G::CW;            // 2 x QSEG
-    float4* v1 = reinterpret_cast<float4*>(qbuf + 2 * G::QSEG);  // MY x NQT
-    float4* v2 = v1 + MY * G::NQT;                                // MY x NT
+    uint64_t* ready = empty + SS;
+    uint64_t* qfull = ready + SS;
+    uint64_t* qempty = qfull + QR;
+    float* uring = reinterpret_cast<float*>(smem_raw + 512);
+    float* qbuf = uring + S * G::USEG;                            // ring of QR q rows
+    float4* v1 = reinterpret_cast<float4*>(qbuf + QR * G::QSEG);  // MY x NT
+    float4* v2 = v1 + MY * NT;                                    // MY x NT
 
     const int tid = threadIdx.x;
     const int x0 = blockIdx.x * G::CW;
@@ -134,184 +183,266 @@ __global__ void __launch_bounds__(FG<RX, RY, NT>::NCT + 32) k_fused(const FusedA
     const int yb1 = min(a.H, yb0 + a.band);
     if (yb0 >= yb1) return;
     const long long img = (long long)blockIdx.z * a.bstride;
+    const long long pitch = a.pitch;
     const int qr_lo = max(0, yb0 - RY), qr_hi = min(a.H - 1, yb1 - 1 + RY);
-    const int j0 = qr_lo - RY;                 // first streamed u row (may be < 0: clamped)
-    const int steps = (yb1 - 1 + 2 * RY) - j0 + 1;
+    const int nq = qr_hi - qr_lo + 1;  // q rows this band needs
+    const int j0 = qr_lo - RY;         // first streamed u row (may be < 0: clamped)
+    const int steps = nq + 2 * RY;     // u rows streamed: j0 .. qr_hi + RY
+    const int useg0 = x0 - 2 * G::HX;  // image column of u-segment index 0
+    // the u segment reaches outside the image: replicate columns 0 / W-1 there
+    const bool edge_cta = useg0 < 0 || x0 + G::CW + 2 * G::HX > a.W;
 
     if (tid == 0) {
         for (int s = 0; s < SS; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], G::NCT / 32);
+            mbar_init(&empty[s], NT);  // every A thread arrives
+            mbar_init(&ready[s], 32);
+        }
+        for (int r = 0; r < QR; ++r) {
+            mbar_init(&qfull[r], NT);   // A threads publish a q row
+            mbar_init(&qempty[r], NT);  // B threads are done reading it
         }
         mbar_fence_init();
     }
     __syncthreads();
 
-    if (tid >= G::NCT) {  // producer warp
-        if (tid == G::NCT) {
-            const int uc0 = max(0, x0 - 2 * G::HX), uc1 = min(a.Wp4, x0 + G::CW + 2 * G::HX);
-            const unsigned ubytes = (unsigned)(uc1 - uc0) * 4u;
-            const int udst = uc0 - (x0 - 2 * G::HX);
-            const int fc0 = max(0, x0 - G::HX), fc1 = min(a.Wp4, x0 + G::CW + G::HX);
-            const unsigned fbytes = (unsigned)(fc1 - fc0) * 4u;
-            const int fdst = fc0 - (x0 - G::HX);
-            const unsigned abytes = (unsigned)(min(a.Wp4, x0 + G::CW) - x0) * 4u;
-            for (int i0 = 0, st = 0; i0 < steps; i0 += R, ++st) {
-                const int s = st % SS;
-                if (st >= SS) mbar_wait(&empty[s], ((st / SS) - 1) & 1);
-                const int nr = min(R, steps - i0);
-                unsigned bytes = 0;
+    if (tid >= 2 * NT) {  // ------------------------------------ producer warp
+        const int lane = tid - 2 * NT;
+        const int nst = (steps + R - 1) / R;
+        const int uc0 = max(0, useg0), uc1 = min(a.Wp4, x0 + G::CW + 2 * G::HX);
+        const unsigned ubytes = (unsigned)(uc1 - uc0) * 4u;
+        const int udst = uc0 - useg0;
+        const int fc0 = max(0, x0 - G::HX), fc1 = min(a.Wp4, x0 + G::CW + G::HX);
+        const unsigned fbytes = (unsigned)(fc1 - fc0) * 4u;
+        auto issue = [&](int st) {
+            const int s = st % SS;
+            if (st >= SS) mbar_wait_sleep(&empty[s], ((st / SS) - 1) & 1, 200);
+            const int nr = min(R, steps - st * R);
+            mbar_arrive_expect_tx(&full[s], ubytes * nr);
+            for (int r = 0; r < nr; ++r) {
+                const int j = j0 + st * R + r;
+                bulk_g2s(uring + (size_t)(s * R + r) * G::USEG + udst,
+                         a.u_in + img + (long long)clampi(j, 0, a.H - 1) * pitch + uc0, ubytes, &full[s]);
+                if (j - RY >= qr_lo && j - RY <= qr_hi)
+                    l2_prefetch(a.f + img + (long long)(j - RY) * pitch + fc0, fbytes);
+            }
+        };
+        if (!edge_cta) {
+            if (lane == 0)
+                for (int st = 0; st < nst; ++st) issue(st);
+            return;
+        }
+        const int lo_end = max(0, -useg0);       // segment indices [0, lo_end) are left of column 0
+        const int hi_beg = max(0, a.W - useg0);  // [hi_beg, UW) are right of column W-1
+        const int i0c = lo_end, iWc = a.W - 1 - useg0;
+        for (int st = 0; st < nst + LAG; ++st) {
+            if (st < nst && lane == 0) issue(st);
+            const int sd = st - LAG;
+            if (sd >= 0 && sd < nst) {
+                const int s = sd % SS;
+                mbar_wait(&full[s], (sd / SS) & 1);
+                const int nr = min(R, steps - sd * R);
                 for (int r = 0; r < nr; ++r) {
-                    const int j = j0 + i0 + r;
-                    bytes += ubytes;
-                    if (j - RY >= qr_lo && j - RY <= qr_hi) bytes += fbytes;
-                    if (j - 2 * RY >= yb0 && j - 2 * RY < yb1) bytes += abytes;
+                    float* seg = uring + (size_t)(s * R + r) * G::USEG;
+                    const float vl = lo_end > 0 ? seg[i0c] : 0.f;
+                    const float vr = hi_beg < G::UW ? seg[iWc] : 0.f;
+                    __syncwarp();
+                    for (int p = lane; p < lo_end; p += 32) seg[p] = vl;
+                    for (int p = hi_beg + lane; p < G::UW; p += 32) seg[p] = vr;
                 }
-                mbar_arrive_expect_tx(&full[s], bytes);
-                for (int r = 0; r < nr; ++r) {
-                    const int j = j0 + i0 + r;
-                    const int slot = s * R + r;
-                    bulk_g2s(uring + (size_t)slot * G::USEG + udst,
-                             a.u_in + img + (long long)clampi(j, 0, a.H - 1) * a.pitch + uc0, ubytes, &full[s]);
-                    if (j - RY >= qr_lo && j - RY <= qr_hi)
-                        bulk_g2s(fring + (size_t)slot * G::QSEG + fdst,
-                                 a.f + img + (long long)(j - RY) * a.pitch + fc0, fbytes, &full[s]);
-                    if (j - 2 * RY >= yb0 && j - 2 * RY < yb1)
-                        bulk_g2s(aring + (size_t)slot * G::CW,
-                                 a.u_in + img + (long long)(j - 2 * RY) * a.pitch + x0, abytes, &full[s]);
-                }
+                __syncwarp();
+                mbar_arrive(&ready[s]);
             }
         }
         return;
     }
 
-    // ---------------------------------------------------------- consumers
-    const int lane = tid & 31;
-    const bool doA = tid < G::NQT, doB = tid < NT;
-    const int qc = x0 - G::HX + 4 * tid;  // first q column of this thread (stage A)
-    const int oc = x0 + 4 * tid;          // first output column (stage B)
-    // warp-uniform edge decisions
-    const int wfirstA = x0 - G::HX + 128 * (tid >> 5);
-    const bool edgeA = (wfirstA - RX < 0) || (wfirstA + 127 + RX > a.W - 1) || (wfirstA < 0) || (wfirstA + 127 > a.W - 1);
-    const int wfirstB = x0 + 128 * (tid >> 5);
-    const bool edgeB = (wfirstB - RX < 0) || (wfirstB + 127 + RX > a.W - 1);
-    const bool full_store = oc + 3 < a.W;
+    auto qrow_ptr = [&](int r) { return qbuf + (size_t)(r & (QR - 1)) * G::QSEG; };
     const float scale = a.scale, eps = a.eps;
-    float4 col1 = make_float4(0.f, 0.f, 0.f, 0.f), col2 = make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 hlast = make_float4(0.f, 0.f, 0.f, 0.f);
-    int n1 = 0, n2 = 0;  // rows pushed into the vertical rings
-    float maxd = 0.f, csum = 0.f;
-    float* outp = a.u_out + img + (long long)yb0 * a.pitch + oc;
-    int s = 0, rr = 0;
-    unsigned phase = 0;
 
-    for (int i = 0; i < steps; ++i) {
-        const int j = j0 + i;
-        if (rr == 0) mbar_wait(&full[s], phase);
-        const int slot = s * R + rr;
-        const int qrow = j - RY;
-        const bool makeq = qrow >= qr_lo && qrow <= qr_hi;
-        float* qb = qbuf + (i & 1) * G::QSEG;
-        // ---- stage A: H1 of u row j, vertical window -> q row j - RY
-        if (doA) {
-            const float* useg = uring + (size_t)slot * G::USEG;
-            const float4 h = edgeA ? hsum_clamped<G::MX>(useg, x0 - 2 * G::HX, qc, RX, a.W, true)
-                                   : hsum_fast<G::MX, G::OFF>(useg, tid);
-            float4* rs = v1 + (size_t)(n1 % MY) * G::NQT + tid;
-            if (n1 >= MY) sub4(col1, *rs);
-            add4(col1, h);
-            *rs = h;
-            ++n1;
-            if (n1 > MY && (n1 & (REFRESH - 1)) == 0) {
-                float4 fr = v1[tid];
-                for (int k = 1; k < MY; ++k) add4(fr, v1[(size_t)k * G::NQT + tid]);
-                col1 = fr;
-            }
-            if (makeq) {
-                const float* fseg = fring + (size_t)slot * G::QSEG;
-                float4 fv = *reinterpret_cast<const float4*>(fseg + 4 * tid);
-                if (edgeA) {  // q columns outside the image take the clamped column's f
-                    float fx[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) fx[e] = fseg[clampi(qc + e, 0, a.W - 1) - (x0 - G::HX)];
-                    fv = make_float4(fx[0], fx[1], fx[2], fx[3]);
-                }
-                const float d0 = col1.x * scale, d1 = col1.y * scale, d2 = col1.z * scale, d3 = col1.w * scale;
-                float4 q;
-                q.x = div_fast(fv.x, d0 < eps ? eps : d0);
-                q.y = div_fast(fv.y, d1 < eps ? eps : d1);
-                q.z = div_fast(fv.z, d2 < eps ? eps : d2);
-                q.w = div_fast(fv.w, d3 < eps ? eps : d3);
-                *reinterpret_cast<float4*>(qb + 4 * tid) = q;
-            }
-        }
-        named_bar(1, G::NCT);
-        // ---- stage B: H2 of q row, pushed into the vertical window
-        if (doB) {
-            int pushes = 0;
-            if (makeq) {
-                hlast = edgeB ? hsum_clamped<G::MX>(qb, x0 - G::HX, oc, RX, a.W, false)
-                              : hsum_fast<G::MX, G::OFF>(qb, tid);
-                pushes = (qrow == qr_lo) ? qr_lo - (yb0 - RY) + 1 : 1;
-            } else if (qrow > qr_hi) {
-                pushes = 1;  // replicate the last q row below the image
-            }
-            for (int p = 0; p < pushes; ++p) {
-                float4* rs = v2 + (size_t)(n2 % MY) * NT + tid;
-                if (n2 >= MY) sub4(col2, *rs);
-                add4(col2, hlast);
-                *rs = hlast;
-                ++n2;
-                if (n2 > MY && (n2 & (REFRESH - 1)) == 0) {
-                    float4 fr = v2[tid];
-                    for (int k = 1; k < MY; ++k) add4(fr, v2[(size_t)k * NT + tid]);
-                    col2 = fr;
-                }
-                if (n2 >= MY) {  // output row yb0 + n2 - MY complete
-                    const float* ax = aring + (size_t)slot * G::CW + 4 * tid;
-                    float4 u = *reinterpret_cast<const float4*>(ax);
-                    float4 c = make_float4(col2.x * scale, col2.y * scale, col2.z * scale, col2.w * scale);
-                    if (!full_store) {
-                        if (oc >= a.W) c.x = u.x = 0.f;
-                        if (oc + 1 >= a.W) c.y = u.y = 0.f;
-                        if (oc + 2 >= a.W) c.z = u.z = 0.f;
-                        c.w = u.w = 0.f;
-                    }
-                    float val[4] = {c.x * u.x, c.y * u.y, c.z * u.z, c.w * u.w};
-                    const float uo[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        if (a.clamp && val[e] < 0.f) val[e] = 0.f;
-                        maxd = fmaxf(maxd, fabsf(val[e] - uo[e]));
-                        csum += val[e];
-                    }
-                    if (full_store) {
-                        *reinterpret_cast<float4*>(outp) = make_float4(val[0], val[1], val[2], val[3]);
-                    } else {
-                        if (oc < a.W) outp[0] = val[0];
-                        if (oc + 1 < a.W) outp[1] = val[1];
-                        if (oc + 2 < a.W) outp[2] = val[2];
-                    }
-                    outp += a.pitch;
+    if (tid < NT) {  // ---------------------------------- A warps: q rows
+        uint64_t* gate = edge_cta ? ready : full;
+        const int qc = x0 - G::HX + 4 * tid;  // first q column of this thread
+        // q columns outside the image take the clamped column's value: such a
+        // thread computes the 4-column group qcl holding the clamped columns
+        // and picks components (warp-uniform)
+        const int wq0 = x0 - G::HX + 128 * (tid >> 5);
+        const bool edgeA = wq0 < 0 || wq0 + 127 > a.W - 1;
+        const int qcl = min(max(qc, 0), (a.W - 1) & ~3);
+        const int4 sel = make_int4(clampi(qc, 0, a.W - 1) - qcl, clampi(qc + 1, 0, a.W - 1) - qcl,
+                                   clampi(qc + 2, 0, a.W - 1) - qcl, clampi(qc + 3, 0, a.W - 1) - qcl);
+        const int chunk = (qcl - qc) / 4 + tid;
+        const float* fcol = a.f + img + qcl;
+        VRing<MY> r1;
+        int s = 0;
+        unsigned phase = 0;
+        // f for A(i): row j0 + i - RY (clamped: prefetches past the band are unused)
+        auto load_f = [&](int i) { return ldg4(fcol + clampi(j0 + i - RY, qr_lo, qr_hi) * pitch); };
+        // step i: u row j0 + i -> H1 -> vertical window -> q row i - 2 RY.
+        // Steady (ST): ring full, a q row every step, the q slot was used
+        // before, parity ODD known at compile time.
+        auto step = [&](auto steady, auto odd, const int i, float4& fx) {
+            constexpr bool ST = decltype(steady)::value;
+            constexpr int ODD = decltype(odd)::value;
+            const bool par = ST ? ODD : (i & 1);
+            if (!par) mbar_wait(&gate[s], phase);
+            float4 h = hsum_fast<G::MX, G::OFF>(uring + (size_t)(s * R + par) * G::USEG, chunk);
+            if (par || (!ST && i == steps - 1)) {  // this thread is done with the stage's u rows
+                mbar_arrive(&empty[s]);
+                if (++s == SS) {
+                    s = 0;
+                    phase ^= 1u;
                 }
             }
-        }
-        if (++rr == R || i == steps - 1) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-            rr = 0;
-            if (++s == SS) {
-                s = 0;
-                phase ^= 1u;
+            if (edgeA) h = pick4(h, sel);
+            if (ST)
+                r1.push_full(v1, NT, tid, h);
+            else
+                r1.push(v1, NT, tid, h);
+            const int r = i - 2 * RY;
+            if (ST || r >= 0) {
+                const float4 fv = edgeA ? pick4(fx, sel) : fx;
+                // f / max(v, eps): max.NaN keeps the reference's NaN propagation
+                const float4 q = make_float4(div_fast(fv.x, fmax_nan(r1.col.x * scale, eps)),
+                                             div_fast(fv.y, fmax_nan(r1.col.y * scale, eps)),
+                                             div_fast(fv.z, fmax_nan(r1.col.z * scale, eps)),
+                                             div_fast(fv.w, fmax_nan(r1.col.w * scale, eps)));
+                if (ST || r >= QR) mbar_wait(&qempty[r & (QR - 1)], ((r / QR) - 1) & 1);
+                *reinterpret_cast<float4*>(qrow_ptr(r) + 4 * tid) = q;
+                mbar_arrive(&qfull[r & (QR - 1)]);
             }
+            if (!ST) fx = load_f(i + 2);
+        };
+        float4 F0 = load_f(0), F1 = load_f(1);
+        const int i_s = 2 * RY + QR;  // ring full, q rows past the first ring turn
+        // steady blocks end 2 rows before the last q row (prefetch stays in range)
+        const int nblk = steps - 2 > i_s ? (steps - 2 - i_s) / REFRESH : 0;
+        int i = 0;
+        for (; i < (nblk ? i_s : steps); i += 2) {
+            step(std::false_type(), std::integral_constant<int, 0>(), i, F0);
+            if (i + 1 < steps) step(std::false_type(), std::integral_constant<int, 1>(), i + 1, F1);
         }
+        if (nblk) {
+            const float* fp = fcol + (long long)(j0 + i + 2 - RY) * pitch;  // f row of A(i + 2)
+            for (int b = 0; b < nblk; ++b) {
+#pragma unroll 1
+                for (int t = 0; t < REFRESH; t += 2, i += 2) {
+                    step(std::true_type(), std::integral_constant<int, 0>(), i, F0);
+                    F0 = ldg4(fp);
+                    step(std::true_type(), std::integral_constant<int, 1>(), i + 1, F1);
+                    F1 = ldg4(fp + pitch);
+                    fp += 2 * pitch;
+                }
+                r1.refresh(v1, NT, tid);  // fp32 drift
+            }
+            r1.n += nblk * REFRESH;
+        }
+        for (; i < steps; i += 2) {
+            step(std::false_type(), std::integral_constant<int, 0>(), i, F0);
+            if (i + 1 < steps) step(std::false_type(), std::integral_constant<int, 1>(), i + 1, F1);
+        }
+        return;
     }
+
+    // ------------------------------------------------ B warps: output rows
+    const int tb = tid - NT;
+    const int lane = tid & 31;
+    const int oc = x0 + 4 * tb;
+    const bool has_out = tb < G::NB && oc < a.W;  // lanes past the strip compute, never store
+    const bool full_store = oc + 3 < a.W;
+    const int ocl = min(oc, a.Wp4 - 4);
+    const float* ucol = a.u_in + img + ocl;
+    float* ocol = a.u_out + img + oc;
+    VRing<MY> r2;
+    float4 hlast = make_float4(0.f, 0.f, 0.f, 0.f);
+    float maxd = 0.f;
+    auto load_u = [&](int o) { return ldg4(ucol + min(yb0 + o, yb1 - 1) * pitch); };  // u of output o
+    auto store = [&](auto fs, const int o, const float4 c, const float4 u) {
+        constexpr bool FS = decltype(fs)::value;
+        const bool fst = FS || full_store;
+        float val[4] = {c.x * scale * u.x, c.y * scale * u.y, c.z * scale * u.z, c.w * scale * u.w};
+        const float uo[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (a.clamp) val[e] = fmax_nan(val[e], 0.f);
+            if (fst || oc + e < a.W) maxd = fmax_nan(maxd, fabsf(val[e] - uo[e]));
+        }
+        float* outp = ocol + (yb0 + o) * pitch;
+        if (fst) {
+            *reinterpret_cast<float4*>(outp) = make_float4(val[0], val[1], val[2], val[3]);
+        } else {
+            outp[0] = val[0];
+            if (oc + 1 < a.W) outp[1] = val[1];
+            if (oc + 2 < a.W) outp[2] = val[2];
+        }
+    };
+    auto take = [&](int r) {  // H2 of q row r (waits for the A warps, frees the slot)
+        mbar_wait_sleep(&qfull[r & (QR - 1)], (r / QR) & 1, FDG_QSLEEP);
+        const float4 h = hsum_fast<G::MX, G::OFF>(qrow_ptr(r), tb);
+        mbar_arrive(&qempty[r & (QR - 1)]);
+        return h;
+    };
+    // pushes: q rows above the image replicate row 0 (extras), rows below
+    // the image replicate the last one (trailing); output o = push - 2 RY
+    const int extras = qr_lo - (yb0 - RY);
+    const int band = yb1 - yb0;
+    auto push_out = [&](const float4 h, float4 u) {
+        r2.push(v2, NT, tb, h);
+        if (r2.n >= MY && has_out) store(std::false_type(), r2.n - MY, r2.col, u);
+    };
+    // warm-up: q rows 0 .. r_s-1 (ring not yet full)
+    const int r_s = (max(1, 2 * RY + 1 - extras) + 1) & ~1;
+    const int r_e = nq;  // steady: one push and one output per q row
+    const int nblk = r_e > r_s ? (r_e - r_s) / REFRESH : 0;
+    int r = 0;
+    for (; r < min(r_s, nq); ++r) {
+        hlast = take(r);
+        if (r == 0)
+            for (int p = 0; p < extras; ++p) r2.push(v2, NT, tb, hlast);
+        const int o = r2.n + 1 - MY;
+        push_out(hlast, o >= 0 ? load_u(o) : make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+    if (nblk) {
+        // here r2 is full and output o = r + extras - 2 RY follows every push
+        const int o0 = r + extras - 2 * RY;
+        float4 U0 = load_u(o0), U1 = load_u(o0 + 1);
+        auto blocks = [&](auto fs) {
+            for (int b = 0; b < nblk; ++b) {
+#pragma unroll 1
+                for (int t = 0; t < REFRESH; t += 2, r += 2) {
+                    const int o = r + extras - 2 * RY;
+                    const float4 g0 = take(r);
+                    const float4 g1 = take(r + 1);
+                    r2.push_full(v2, NT, tb, g0);
+                    if (has_out) store(fs, o, r2.col, U0);
+                    r2.push_full(v2, NT, tb, g1);
+                    if (has_out) store(fs, o + 1, r2.col, U1);
+                    U0 = load_u(o + 2);
+                    U1 = load_u(o + 3);
+                    hlast = g1;
+                }
+                r2.refresh(v2, NT, tb);  // fp32 drift
+            }
+        };
+        if (x0 + G::CW <= a.W)
+            blocks(std::true_type());  // every B lane owns 4 image columns
+        else
+            blocks(std::false_type());
+        r2.n += nblk * REFRESH;
+    }
+    for (; r < nq; ++r) {
+        hlast = take(r);
+        push_out(hlast, load_u(r2.n + 1 - MY));
+    }
+    while (r2.n - 2 * RY < band) push_out(hlast, load_u(r2.n + 1 - MY));  // below the image
+
     if (a.maxchange) {
-        const unsigned bits = __reduce_max_sync(0xffffffffu, __float_as_uint(maxd));
-        const int nan = __reduce_or_sync(0xffffffffu, (int)isnan(csum));
+        const bool nan = isnan(maxd);
+        const unsigned bits = __reduce_max_sync(0xffffffffu, nan ? 0u : __float_as_uint(maxd));
+        const int anynan = __reduce_or_sync(0xffffffffu, (int)nan);
         if (lane == 0) {
             if (bits) atomicMax(a.maxchange, bits);
-            if (nan) atomicOr(a.nanflag, 1);
+            if (anynan) atomicOr(a.nanflag, 1);
         }
     }
 }
@@ -319,11 +450,9 @@ __global__ void __launch_bounds__(FG<RX, RY, NT>::NCT + 32) k_fused(const FusedA
 template <int RX, int RY, int NT, int R, int S>
 size_t smem_bytes() {
     using G = FG<RX, RY, NT>;
-    return 256 + sizeof(float) * ((size_t)S * G::USEG + (size_t)S * G::QSEG + (size_t)S * G::CW + 2 * (size_t)G::QSEG) +
-           sizeof(float4) * ((size_t)G::MY * G::NQT + (size_t)G::MY * NT);
+    return 512 + sizeof(float) * ((size_t)S * G::USEG + 8 * (size_t)G::QSEG) + sizeof(float4) * 2 * (size_t)G::MY * NT;
 }
 
-// Band height: whole waves of resident CTAs (one CTA per band x strip x image).
 template <int RX, int RY, int NT, int R, int S>
 cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     using G = FG<RX, RY, NT>;
@@ -332,7 +461,7 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     if (err != cudaSuccess) return err;
     static int occ = 0;
     if (!occ) {
-        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused<RX, RY, NT, R, S>, G::NCT + 32, smem);
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused<RX, RY, NT, R, S>, 2 * NT + 32, smem);
         if (err != cudaSuccess) return err;
         if (occ < 1) occ = 1;
     }
@@ -350,15 +479,15 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     a.band = (int)((a.H + ctas_y - 1) / ctas_y);
     if (const char* e = getenv("FDG_FUSED_BAND")) a.band = std::max(1, atoi(e));
     dim3 grid(strips, (a.H + a.band - 1) / a.band, a.batch);
-    k_fused<RX, RY, NT, R, S><<<grid, G::NCT + 32, smem, st>>>(a);
+    k_fused<RX, RY, NT, R, S><<<grid, 2 * NT + 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 
-}  // namespace
-
 // Engine selection: 0 = off (default until it beats the two-pass engine on
 // config 4), 1 = on; FDG_FUSED=0/1 or fdg_set_option("fused", v).
-static int g_fused = getenv("FDG_FUSED") ? atoi(getenv("FDG_FUSED")) : 0;
+int g_fused = getenv("FDG_FUSED") ? atoi(getenv("FDG_FUSED")) : 0;
+
+}  // namespace
 
 void set_fused_mode(int v) { g_fused = v; }
 int fused_mode() { return g_fused; }
@@ -387,10 +516,9 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
     a.nanflag = nanflag;
     static const int variant = getenv("FDG_FUSED_V") ? atoi(getenv("FDG_FUSED_V")) : 0;
     switch (variant) {
-        case 1: return launch_t<7, 7, 128, 2, 4>(a, st);
-        case 2: return launch_t<7, 7, 64, 4, 8>(a, st);
-        case 3: return launch_t<7, 7, 64, 2, 4>(a, st);
-        default: return launch_t<7, 7, 128, 4, 8>(a, st);
+        case 1: return launch_t<7, 7, 128, 2, 16>(a, st);
+        case 2: return launch_t<7, 7, 64, 2, 16>(a, st);
+        default: return launch_t<7, 7, 128, 2, 12>(a, st);
     }
 }
 
