@@ -94,7 +94,7 @@ const char* fdg_last_error(void);
 int fdg_device_available(void);
 /* Process-wide engine options (no reference counterpart; tuning/testing):
  *   "fused": 1 = run each RL iteration of the centred 15x15 box as one fused
- *            pass (kernels_fused.cu), 0 = two fused-epilogue passes (default).
+ *            pass (kernels_fused.cu, default), 0 = two fused-epilogue passes.
  * Returns the previous value, or -1 for an unknown name. */
 int fdg_set_option(const char* name, int value);
 

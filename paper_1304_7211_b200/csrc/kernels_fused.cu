@@ -69,28 +69,38 @@ struct FusedArgs {
     int* nanflag;
 };
 
-template <int MX, int OFF>
-__device__ __forceinline__ float4 hsum_fast(const float* seg, int chunk) {
-    constexpr int NCH = (OFF + 3 + MX - 1) / 4 + 1;
-    float v[4 * NCH];
+// ---- packed fp32x2 arithmetic (Blackwell FADD2 / FMUL2 / FFMA2)
+__device__ __forceinline__ float2 lo2(const float4 v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4 v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float4 cat4(const float2 a, const float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
+__device__ __forceinline__ float2 add2(const float2 a, const float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(const float2 a, const float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(const float2 a, const float2 b, const float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float4 add4(const float4 a, const float4 b) {
+    return cat4(add2(lo2(a), lo2(b)), add2(hi2(a), hi2(b)));
+}
+__device__ __forceinline__ float4 sub4(const float4 a, const float4 b) {
+    return cat4(add2(lo2(a), make_float2(-b.x, -b.y)), add2(hi2(a), make_float2(-b.z, -b.w)));
+}
+__device__ __forceinline__ float4 mul4s(const float4 a, const float s) {
+    const float2 ss = make_float2(s, s);
+    return cat4(mul2(lo2(a), ss), mul2(hi2(a), ss));
+}
+
+// 15-wide window sums of 4 consecutive columns, packed: window e covers
+// v[1+e .. 15+e] of the 5 float4 chunks starting at `chunk`.
+__device__ __forceinline__ float4 hsum15x4(const float* seg, int chunk) {
     const float4* p = reinterpret_cast<const float4*>(seg) + chunk;
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-        const float4 q = p[c];
-        v[4 * c] = q.x;
-        v[4 * c + 1] = q.y;
-        v[4 * c + 2] = q.z;
-        v[4 * c + 3] = q.w;
-    }
-    static_assert(MX == 15, "tree below is written for 15-wide windows");
-    // shared middle v[OFF+3 .. OFF+14] as a balanced tree (short dependency chain)
-    const float m01 = (v[OFF + 3] + v[OFF + 4]) + (v[OFF + 5] + v[OFF + 6]);
-    const float m23 = (v[OFF + 7] + v[OFF + 8]) + (v[OFF + 9] + v[OFF + 10]);
-    const float m45 = (v[OFF + 11] + v[OFF + 12]) + (v[OFF + 13] + v[OFF + 14]);
-    const float mid = (m01 + m23) + m45;
-    const float l2 = v[OFF + 2], l1 = v[OFF + 1] + l2, l0 = v[OFF] + l1;
-    const float r1 = v[OFF + MX], r2 = r1 + v[OFF + MX + 1], r3 = r2 + v[OFF + MX + 2];
-    return make_float4(l0 + mid, (l1 + mid) + r1, (l2 + mid) + r2, mid + r3);
+    const float4 c0 = p[0], c1 = p[1], c2 = p[2], c3 = p[3], c4 = p[4];
+    // shared middle v[4..15] = chunks 1..3 as six pairs, tree-summed
+    const float2 m = add2(add2(add2(lo2(c1), hi2(c1)), add2(lo2(c2), hi2(c2))), add2(lo2(c3), hi2(c3)));
+    const float mid = m.x + m.y;
+    const float a = c0.z + c0.w;  // v2 + v3
+    const float b = c4.x + c4.y;  // v16 + v17
+    const float2 mm = make_float2(mid, mid);
+    const float2 o01 = add2(add2(make_float2(c0.y, c4.x), make_float2(a, a)), mm);  // v1 + a, v16 + a
+    const float2 o23 = add2(add2(make_float2(c0.w, c4.z), make_float2(b, b)), mm);  // v3 + b, v18 + b
+    return cat4(o01, o23);
 }
 
 // component k (0..3) of v, for the q columns outside the image that take the
@@ -123,33 +133,21 @@ struct VRing {
     __device__ __forceinline__ void push_full(float4* ring, int stride, int t, const float4 h) {
         float4* rs = ring + (size_t)slot * stride + t;
         const float4 o = *rs;
-        col.x = (col.x - o.x) + h.x;
-        col.y = (col.y - o.y) + h.y;
-        col.z = (col.z - o.z) + h.z;
-        col.w = (col.w - o.w) + h.w;
+        col = add4(sub4(col, o), h);
         *rs = h;
         slot = slot + 1 == MY ? 0 : slot + 1;
     }
     __device__ __forceinline__ void refresh(const float4* ring, int stride, int t) {
         float4 fr = ring[t];
 #pragma unroll
-        for (int k = 1; k < MY; ++k) {
-            const float4 o = ring[(size_t)k * stride + t];
-            fr.x += o.x;
-            fr.y += o.y;
-            fr.z += o.z;
-            fr.w += o.w;
-        }
+        for (int k = 1; k < MY; ++k) fr = add4(fr, ring[(size_t)k * stride + t]);
         col = fr;
     }
     __device__ __forceinline__ void push(float4* ring, int stride, int t, const float4 h) {
         if (n >= MY) {
             push_full(ring, stride, t, h);
         } else {
-            col.x += h.x;
-            col.y += h.y;
-            col.z += h.z;
-            col.w += h.w;
+            col = add4(col, h);
             ring[(size_t)slot * stride + t] = h;
             slot = slot + 1 == MY ? 0 : slot + 1;
         }
@@ -162,6 +160,7 @@ template <int RX, int RY, int NT, int R, int S>
 __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     using G = FG<RX, RY, NT>;
     static_assert(R == 2, "stage logic assumes two rows per stage");
+    static_assert(G::MX == 15 && G::OFF == 1, "hsum15x4 reads 5 chunks, window at offset 1");
     constexpr int SS = S / R;
     constexpr int LAG = SS / 2;  // edge CTAs: the producer readies stage st - LAG
     constexpr int MY = G::MY;
@@ -281,12 +280,27 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         // step i: u row j0 + i -> H1 -> vertical window -> q row i - 2 RY.
         // Steady (ST): ring full, a q row every step, the q slot was used
         // before, parity ODD known at compile time.
+        // q = f / max(v, eps) with v = col / (MX MY): max.NaN keeps the
+        // reference's NaN propagation; MUFU reciprocal + one Newton step (packed)
+        auto quot4 = [&](const float4 col, const float4 fv) {
+            const float4 v = mul4s(col, scale);
+            const float4 d = make_float4(fmax_nan(v.x, eps), fmax_nan(v.y, eps), fmax_nan(v.z, eps), fmax_nan(v.w, eps));
+            float4 r;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(d.x));
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(d.y));
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.z) : "f"(d.z));
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.w) : "f"(d.w));
+            const float2 q0l = mul2(lo2(fv), lo2(r)), q0h = mul2(hi2(fv), hi2(r));
+            const float2 el = fma2(make_float2(-d.x, -d.y), q0l, lo2(fv));
+            const float2 eh = fma2(make_float2(-d.z, -d.w), q0h, hi2(fv));
+            return cat4(fma2(el, lo2(r), q0l), fma2(eh, hi2(r), q0h));
+        };
         auto step = [&](auto steady, auto odd, const int i, float4& fx) {
             constexpr bool ST = decltype(steady)::value;
             constexpr int ODD = decltype(odd)::value;
             const bool par = ST ? ODD : (i & 1);
             if (!par) mbar_wait(&gate[s], phase);
-            float4 h = hsum_fast<G::MX, G::OFF>(uring + (size_t)(s * R + par) * G::USEG, chunk);
+            float4 h = hsum15x4(uring + (size_t)(s * R + par) * G::USEG, chunk);
             if (par || (!ST && i == steps - 1)) {  // this thread is done with the stage's u rows
                 mbar_arrive(&empty[s]);
                 if (++s == SS) {
@@ -303,10 +317,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
             if (ST || r >= 0) {
                 const float4 fv = edgeA ? pick4(fx, sel) : fx;
                 // f / max(v, eps): max.NaN keeps the reference's NaN propagation
-                const float4 q = make_float4(div_fast(fv.x, fmax_nan(r1.col.x * scale, eps)),
-                                             div_fast(fv.y, fmax_nan(r1.col.y * scale, eps)),
-                                             div_fast(fv.z, fmax_nan(r1.col.z * scale, eps)),
-                                             div_fast(fv.w, fmax_nan(r1.col.w * scale, eps)));
+                const float4 q = quot4(r1.col, fv);
                 if (ST || r >= QR) mbar_wait(&qempty[r & (QR - 1)], ((r / QR) - 1) & 1);
                 *reinterpret_cast<float4*>(qrow_ptr(r) + 4 * tid) = q;
                 mbar_arrive(&qfull[r & (QR - 1)]);
@@ -360,13 +371,16 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     auto store = [&](auto fs, const int o, const float4 c, const float4 u) {
         constexpr bool FS = decltype(fs)::value;
         const bool fst = FS || full_store;
-        float val[4] = {c.x * scale * u.x, c.y * scale * u.y, c.z * scale * u.z, c.w * scale * u.w};
-        const float uo[4] = {u.x, u.y, u.z, u.w};
+        const float4 cu = mul4s(c, scale);
+        float4 v4 = cat4(mul2(lo2(cu), lo2(u)), mul2(hi2(cu), hi2(u)));
+        if (a.clamp)
+            v4 = make_float4(fmax_nan(v4.x, 0.f), fmax_nan(v4.y, 0.f), fmax_nan(v4.z, 0.f), fmax_nan(v4.w, 0.f));
+        const float4 dv = sub4(v4, u);
+        float val[4] = {v4.x, v4.y, v4.z, v4.w};
+        const float dd[4] = {dv.x, dv.y, dv.z, dv.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if (a.clamp) val[e] = fmax_nan(val[e], 0.f);
-            if (fst || oc + e < a.W) maxd = fmax_nan(maxd, fabsf(val[e] - uo[e]));
-        }
+        for (int e = 0; e < 4; ++e)
+            if (fst || oc + e < a.W) maxd = fmax_nan(maxd, fabsf(dd[e]));
         float* outp = ocol + (yb0 + o) * pitch;
         if (fst) {
             *reinterpret_cast<float4*>(outp) = make_float4(val[0], val[1], val[2], val[3]);
@@ -378,7 +392,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     };
     auto take = [&](int r) {  // H2 of q row r (waits for the A warps, frees the slot)
         mbar_wait_sleep(&qfull[r & (QR - 1)], (r / QR) & 1, FDG_QSLEEP);
-        const float4 h = hsum_fast<G::MX, G::OFF>(qrow_ptr(r), tb);
+        const float4 h = hsum15x4(qrow_ptr(r), tb);
         mbar_arrive(&qempty[r & (QR - 1)]);
         return h;
     };
@@ -483,9 +497,9 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-// Engine selection: 0 = off (default until it beats the two-pass engine on
-// config 4), 1 = on; FDG_FUSED=0/1 or fdg_set_option("fused", v).
-int g_fused = getenv("FDG_FUSED") ? atoi(getenv("FDG_FUSED")) : 0;
+// Engine selection: 1 = on (default; beats the two-pass engine on config 4),
+// 0 = off; FDG_FUSED=0/1 or fdg_set_option("fused", v).
+int g_fused = getenv("FDG_FUSED") ? atoi(getenv("FDG_FUSED")) : 1;
 
 }  // namespace
 
