@@ -151,7 +151,7 @@ def run_ours(args, cfg, world, rank, local):
     import torch
     import torch.distributed as dist
 
-    from paper_1304_7211_b200 import RlConfig, RlSolver, OperatorKind as K, rlDeconvolve, workloads as W
+    from paper_1304_7211_b200 import ConvPlan, RlConfig, RlSolver, OperatorKind as K, rlDeconvolve, workloads as W
     from paper_1304_7211_b200 import sharded as S
     from paper_1304_7211_b200._lib import Context
 
@@ -240,12 +240,26 @@ def run_ours(args, cfg, world, rank, local):
     total_pxit = W_ * H_ * iters * (cfg.batch if cfg.batch > 1 else 1)
     value = total_pxit / (ms_step * 1e-3) / 1e6
 
-    # pass-kernel duration: one pass = one launch of the dominant kernel
-    passes_per_step = 2 * iters
-    kern_ms = ms_step / passes_per_step  # includes halo exchanges when world > 1
-    kbytes = 12.0 * px_local  # per launch: read conv input + epilogue operand, write output (fp32)
+    # dominant-kernel duration: the step is back-to-back launches of one
+    # engine (two pass launches per iteration, one fused launch per
+    # iteration, or one row-resident launch per run); its average launch time
+    # is the step time over the launches (incl. halo exchanges when world > 1)
+    # (row strips on several ranks run the two-pass solver passes)
+    engine = solver.engine() if world == 1 or cfg.batch > 1 else ConvPlan(psf, op).engine()
+    per_step = max(1, round(launches / max(1, args.steps) / max(1, world)))
+    kern_ms = ms_step / per_step
+    pxit_per_launch = px_local * iters / per_step
+    # algorithmic bytes: SURVEY 8d's canonical 24 B/px*it (two passes x (2
+    # reads + 1 write) x fp32) is kept as the denominator for every engine;
+    # the fused kernel moves 12 B/px*it, the row-resident one 8 B/px per run
+    kbytes = B_PER_PXIT * pxit_per_launch
     peak, peak_kind = peaks()
     achieved = kbytes / (kern_ms * 1e-3) / 1e9
+    hbm_bytes = {"fused": 12.0, "rowres": 8.0 / iters}.get(engine, 24.0)
+    kernel_desc = {"fused": "k_fused (whole RL iteration per launch, 12 B/px*it through HBM)",
+                   "rowres": "k_rowres (all iterations per launch, rows resident in shared memory)",
+                   "box": "k_rect (fused conv + RL epilogue, 12 B/px per pass launch)"}.get(
+        engine, f"k_{engine} (fused conv pass, 12 B/px per pass launch)")
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -294,16 +308,18 @@ def run_ours(args, cfg, world, rank, local):
             "scaling": "strong" if cfg.batch == 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded BASELINE generator)",
             "config": {"workload": cfg.name, "width": W_, "height": H_, "batch": cfg.batch, "psf": cfg.psf,
-                       "op": cfg.op, "iterations": iters, "engine": solver_engine(psf, op),
+                       "op": cfg.op, "iterations": iters, "engine": engine,
                        "parallelism": f"rowstrip{world}" if cfg.batch == 1 else f"image-shard{world}",
                        "l2": "working set 3 planes >> 126 MB L2 (no flush needed)" if W_ * H_ * 12 * nimg > 4e8
                        else "working set L2-resident",
                        "setup_s": round(setup_s, 2)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "k_rect (fused conv + RL epilogue), 12 B/px per launch" if cfg.op.startswith("box")
-                         else "fused conv pass, 12 B/px per launch",
-                         "kernel_ms": kern_ms},
+                         "kernel": kernel_desc, "engine": engine, "kernel_ms": kern_ms,
+                         "launches_per_step": per_step,
+                         "algorithmic_bytes_per_launch": kbytes,
+                         "model": "canonical 24 B/px*it (SURVEY 8d)",
+                         "engine_hbm_bytes_per_pxit": hbm_bytes},
             "hbm_roofline_mpxit": peak * 1e9 / B_PER_PXIT / 1e6 * world,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
@@ -341,14 +357,6 @@ def make_input_gpu(cfg, psf, dev, image=0):
     f = torch.clamp_min(bd + noise, 1e-6)
     torch.cuda.synchronize(dev)
     return f
-
-
-def solver_engine(psf, op):
-    from paper_1304_7211_b200 import ConvPlan
-    try:
-        return ConvPlan(psf, op).engine()
-    except Exception:
-        return None
 
 
 def cpu_baseline(cfg):

@@ -178,6 +178,10 @@ int fdg_solver_pass(fdg_solver* s, int pass, const float* d_in, const float* d_a
                     int iteration);
 /* copy per-iteration {max|du|, NaN} back (synchronises) */
 int fdg_solver_trace(fdg_solver* s, fdg_rl_record* out, int n);
+/* Engine fdg_solver_run uses: "fused" (one launch per iteration), "rowres"
+ * (one launch per run) or the plan engine of the two-pass loop ("box",
+ * "spans", "taps", "dense"). */
+const char* fdg_solver_engine(const fdg_solver* s);
 int fdg_solver_reset_trace(fdg_solver* s);
 
 /* ---- stream compaction (selective path) ------------------------------ */

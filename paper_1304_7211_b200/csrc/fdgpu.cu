@@ -1276,6 +1276,13 @@ int fdg_solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long 
     return FDG_OK;
 }
 
+const char* fdg_solver_engine(const fdg_solver* s) {
+    if (!s) return "?";
+    if (use_rowres(s->fwd.get(), s->W)) return "rowres";
+    if (use_fused(s->fwd.get())) return "fused";
+    return engine_name(s->fwd->dev.engine);
+}
+
 int fdg_solver_trace(fdg_solver* s, fdg_rl_record* out, int n) {
     if (!s || !out) return set_err(FDG_EINVAL, "null argument");
     n = std::min(n, s->ntrace);

@@ -202,6 +202,10 @@ class RlSolver:
     def launches(self) -> int:
         return self.ctx.launch_count()
 
+    def engine(self) -> str:
+        """Engine of run(): "fused", "rowres" or the two-pass plan engine."""
+        return lib().fdg_solver_engine(self.h).decode()
+
     def __del__(self):
         try:
             if self.h:
