@@ -156,7 +156,7 @@ struct VRing {
     }
 };
 
-template <int RX, int RY, int NT, int R, int S>
+template <int RX, int RY, int NT, int R, int S, int QR>
 __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     using G = FG<RX, RY, NT>;
     static_assert(R == 2, "stage logic assumes two rows per stage");
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     constexpr int SS = S / R;
     constexpr int LAG = SS / 2;  // edge CTAs: the producer readies stage st - LAG
     constexpr int MY = G::MY;
-    constexpr int QR = 8;        // q ring rows between the A and B warps
+    static_assert((QR & (QR - 1)) == 0, "q ring rows between the A and B warps: power of two");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     uint64_t* empty = full + SS;
@@ -291,6 +291,9 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
             asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.z) : "f"(d.z));
             asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.w) : "f"(d.w));
             const float2 q0l = mul2(lo2(fv), lo2(r)), q0h = mul2(hi2(fv), hi2(r));
+#ifdef FDG_FUSED_NO_NEWTON
+            return cat4(q0l, q0h);
+#endif
             const float2 el = fma2(make_float2(-d.x, -d.y), q0l, lo2(fv));
             const float2 eh = fma2(make_float2(-d.z, -d.w), q0h, hi2(fv));
             return cat4(fma2(el, lo2(r), q0l), fma2(eh, hi2(r), q0h));
@@ -338,10 +341,41 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
             for (int b = 0; b < nblk; ++b) {
 #pragma unroll 1
                 for (int t = 0; t < REFRESH; t += 2, i += 2) {
+#ifdef FDG_FUSED_STEPWISE
                     step(std::true_type(), std::integral_constant<int, 0>(), i, F0);
                     F0 = ldg4(fp);
                     step(std::true_type(), std::integral_constant<int, 1>(), i + 1, F1);
                     F1 = ldg4(fp + pitch);
+#else
+                    // one stage (2 u rows) per iteration: both window sums in
+                    // flight, then both q rows handed to the B warps
+                    mbar_wait(&gate[s], phase);
+                    const float* us = uring + (size_t)(s * R) * G::USEG;
+                    float4 h0 = hsum15x4(us, chunk);
+                    float4 h1 = hsum15x4(us + G::USEG, chunk);
+                    mbar_arrive(&empty[s]);
+                    if (++s == SS) {
+                        s = 0;
+                        phase ^= 1u;
+                    }
+                    if (edgeA) {
+                        h0 = pick4(h0, sel);
+                        h1 = pick4(h1, sel);
+                    }
+                    r1.push_full(v1, NT, tid, h0);
+                    const float4 qa = quot4(r1.col, edgeA ? pick4(F0, sel) : F0);
+                    r1.push_full(v1, NT, tid, h1);
+                    const float4 qb = quot4(r1.col, edgeA ? pick4(F1, sel) : F1);
+                    F0 = ldg4(fp);
+                    F1 = ldg4(fp + pitch);
+                    const int r = i - 2 * RY;  // even: slots r, r + 1 in the same ring turn
+                    mbar_wait(&qempty[r & (QR - 1)], ((r / QR) - 1) & 1);
+                    mbar_wait(&qempty[(r + 1) & (QR - 1)], (((r + 1) / QR) - 1) & 1);
+                    *reinterpret_cast<float4*>(qrow_ptr(r) + 4 * tid) = qa;
+                    *reinterpret_cast<float4*>(qrow_ptr(r + 1) + 4 * tid) = qb;
+                    mbar_arrive(&qfull[r & (QR - 1)]);
+                    mbar_arrive(&qfull[(r + 1) & (QR - 1)]);
+#endif
                     fp += 2 * pitch;
                 }
                 r1.refresh(v1, NT, tid);  // fp32 drift
@@ -461,21 +495,21 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     }
 }
 
-template <int RX, int RY, int NT, int R, int S>
+template <int RX, int RY, int NT, int R, int S, int QR>
 size_t smem_bytes() {
     using G = FG<RX, RY, NT>;
-    return 512 + sizeof(float) * ((size_t)S * G::USEG + 8 * (size_t)G::QSEG) + sizeof(float4) * 2 * (size_t)G::MY * NT;
+    return 512 + sizeof(float) * ((size_t)S * G::USEG + QR * (size_t)G::QSEG) + sizeof(float4) * 2 * (size_t)G::MY * NT;
 }
 
-template <int RX, int RY, int NT, int R, int S>
+template <int RX, int RY, int NT, int R, int S, int QR>
 cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     using G = FG<RX, RY, NT>;
-    const size_t smem = smem_bytes<RX, RY, NT, R, S>();
-    cudaError_t err = smem_attr<k_fused<RX, RY, NT, R, S>>();
+    const size_t smem = smem_bytes<RX, RY, NT, R, S, QR>();
+    cudaError_t err = smem_attr<k_fused<RX, RY, NT, R, S, QR>>();
     if (err != cudaSuccess) return err;
     static int occ = 0;
     if (!occ) {
-        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused<RX, RY, NT, R, S>, 2 * NT + 32, smem);
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused<RX, RY, NT, R, S, QR>, 2 * NT + 32, smem);
         if (err != cudaSuccess) return err;
         if (occ < 1) occ = 1;
     }
@@ -493,7 +527,7 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     a.band = (int)((a.H + ctas_y - 1) / ctas_y);
     if (const char* e = getenv("FDG_FUSED_BAND")) a.band = std::max(1, atoi(e));
     dim3 grid(strips, (a.H + a.band - 1) / a.band, a.batch);
-    k_fused<RX, RY, NT, R, S><<<grid, 2 * NT + 32, smem, st>>>(a);
+    k_fused<RX, RY, NT, R, S, QR><<<grid, 2 * NT + 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -530,9 +564,9 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
     a.nanflag = nanflag;
     static const int variant = getenv("FDG_FUSED_V") ? atoi(getenv("FDG_FUSED_V")) : 0;
     switch (variant) {
-        case 1: return launch_t<7, 7, 128, 2, 16>(a, st);
-        case 2: return launch_t<7, 7, 64, 2, 16>(a, st);
-        default: return launch_t<7, 7, 128, 2, 12>(a, st);
+        case 1: return launch_t<7, 7, 128, 2, 8, 16>(a, st);
+        case 2: return launch_t<7, 7, 128, 2, 16, 8>(a, st);
+        default: return launch_t<7, 7, 128, 2, 12, 8>(a, st);
     }
 }
 
