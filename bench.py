@@ -34,6 +34,12 @@ sys.path.insert(0, ROOT)
 B_PER_PXIT = 24  # algorithmic HBM bytes per px*it (2 passes x (2 reads + 1 write) x fp32)
 
 
+# FP32 FMA throughput measured on this pool's B200 (scripts/ffma2_probe.cu,
+# profiles/r01_ffma2_probe.md): 74.1 TFLOP/s = 148 SMs x 128 lanes x 2 x 1.965 GHz
+FP32_TFLOPS_MEASURED = 74.1
+DENSE_FLOP_PER_PXIT = 2 * 2 * 961  # two 31x31 correlations, one FMA per tap
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -169,8 +175,9 @@ def run_ours(args, cfg, world, rank, local):
 
     # ---- inputs (built once per rank, then resident in HBM)
     t0 = time.time()
+    fused_strips = world > 1 and cfg.batch == 1 and cfg.psf == "box15x15"  # the fused engine's PSF
     if cfg.batch == 1:
-        halo = S.psf_halo(psf) if world > 1 else 0
+        halo = (S.fused_halo(psf) if fused_strips else S.psf_halo(psf)) if world > 1 else 0
         s = S.strip_of(H_, world, rank, halo)
         f_full = make_input_gpu(cfg, psf, dev)
         f_dev = torch.zeros((s.rows, pitch), dtype=torch.float32, device=dev)
@@ -193,7 +200,12 @@ def run_ours(args, cfg, world, rank, local):
     stream = torch.cuda.current_stream(dev)
     solver.use_stream(stream.cuda_stream)
 
-    if s is not None and world > 1:
+    if s is not None and world > 1 and fused_strips and solver.engine() == "fused":
+        fused = S.GpuFused(solver)
+
+        def step():  # one 2T-row u exchange + one fused launch per iteration
+            S.rl_strips_fused(f_dev, s, iters, fused, u=u_dev, u2=q_dev)
+    elif s is not None and world > 1:
         passes = S.GpuPasses(solver)
 
         def step():
@@ -245,7 +257,7 @@ def run_ours(args, cfg, world, rank, local):
     # iteration, or one row-resident launch per run); its average launch time
     # is the step time over the launches (incl. halo exchanges when world > 1)
     # (row strips on several ranks run the two-pass solver passes)
-    engine = solver.engine() if world == 1 or cfg.batch > 1 else ConvPlan(psf, op).engine()
+    engine = solver.engine() if world == 1 or cfg.batch > 1 or fused_strips else ConvPlan(psf, op).engine()
     per_step = max(1, round(launches / max(1, args.steps) / max(1, world)))
     kern_ms = ms_step / per_step
     pxit_per_launch = px_local * iters / per_step
@@ -267,6 +279,19 @@ def run_ours(args, cfg, world, rank, local):
             traffic = json.load(open(tp)).get(cfg.name)
         except Exception:
             traffic = None
+
+    # the dense 31x31 engine (cfg3) is FP32-FMA bound: its roofline is FLOP/s
+    roof = None
+    if engine == "dense":
+        # one correlation per launch: pxit_per_launch is half an iteration's px*it
+        tf = DENSE_FLOP_PER_PXIT * pxit_per_launch / (kern_ms * 1e-3) / 1e12
+        roof = {"bound": "fp32", "achieved": tf, "peak": FP32_TFLOPS_MEASURED, "unit": "TFLOP/s",
+                "frac": tf / FP32_TFLOPS_MEASURED, "traffic": traffic,
+                "peak_kind": "measured FFMA throughput (profiles/r01_ffma2_probe.md)",
+                "kernel": "k_dense (31x31 correlation + RL epilogue, 2*961 FLOP/px per launch)",
+                "engine": engine, "kernel_ms": kern_ms, "launches_per_step": per_step,
+                "algorithmic_flop_per_launch": DENSE_FLOP_PER_PXIT * pxit_per_launch,
+                "hbm_frac_canonical": achieved / peak}
 
     # ---- e2e through the public host API (rank-local, N = 1 semantics per rank)
     e2e = None
@@ -309,11 +334,12 @@ def run_ours(args, cfg, world, rank, local):
             "data": "synthetic (seeded BASELINE generator)",
             "config": {"workload": cfg.name, "width": W_, "height": H_, "batch": cfg.batch, "psf": cfg.psf,
                        "op": cfg.op, "iterations": iters, "engine": engine,
-                       "parallelism": f"rowstrip{world}" if cfg.batch == 1 else f"image-shard{world}",
+                       "parallelism": (f"rowstrip{world}" + ("-fused" if fused_strips else "")) if cfg.batch == 1
+                       else f"image-shard{world}",
                        "l2": "working set 3 planes >> 126 MB L2 (no flush needed)" if W_ * H_ * 12 * nimg > 4e8
                        else "working set L2-resident",
                        "setup_s": round(setup_s, 2)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "roofline": roof if roof else {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": kernel_desc, "engine": engine, "kernel_ms": kern_ms,
                          "launches_per_step": per_step,

@@ -176,6 +176,13 @@ int fdg_solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long 
 int fdg_solver_pass(fdg_solver* s, int pass, const float* d_in, const float* d_aux, float* d_out,
                     int pitch, long long image_stride, int y0, int y1, int ylo, int yhi,
                     int iteration);
+/* One whole RL iteration with the fused engine (fdg_solver_engine() ==
+ * "fused"): u_out rows [y0, y1) from u_in, reading rows clamped into
+ * [ylo, yhi] (same row convention as fdg_solver_pass; a row strip needs
+ * 2 x (PSF vertical radius) valid halo rows of u_in on each inner side).
+ * u_in != u_out. */
+int fdg_solver_iterate(fdg_solver* s, const float* d_f, const float* d_u_in, float* d_u_out, int pitch,
+                       long long image_stride, int y0, int y1, int ylo, int yhi, int iteration);
 /* copy per-iteration {max|du|, NaN} back (synchronises) */
 int fdg_solver_trace(fdg_solver* s, fdg_rl_record* out, int n);
 /* Engine fdg_solver_run uses: "fused" (one launch per iteration), "rowres"

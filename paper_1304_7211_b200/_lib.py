@@ -108,6 +108,8 @@ def lib():
             "fdg_op_counters": (C.c_int, [D, C.c_int, C.c_int, C.c_int, u64p]),
             "fdg_plan_engine": (C.c_char_p, [vp]),
             "fdg_solver_engine": (C.c_char_p, [vp]),
+            "fdg_solver_iterate": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_longlong, C.c_int, C.c_int, C.c_int,
+                                             C.c_int, C.c_int]),
             "fdg_conv_apply": (C.c_int, [vp, fp, C.c_int, C.c_int, fp]),
             "fdg_conv_apply_masked": (C.c_int, [vp, fp, C.c_int, C.c_int, u8p, fp, fp]),
             "fdg_conv_apply_device": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int]),

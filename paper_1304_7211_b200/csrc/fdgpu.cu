@@ -389,8 +389,11 @@ bool use_fused(const fdg_plan* pl) {
 }
 
 int run_fused(fdg_plan* pl, const float* u_in, const float* f, float* u_out, int pitch, int W, int H, int batch,
-              long long bstride, const fdg_rl_config* cfg, unsigned* mc, int* nf, cudaStream_t st) {
-    cudaError_t r = launch_fused(u_in, f, u_out, pitch, W, H, batch, bstride, pl->dev.scale,
+              long long bstride, const fdg_rl_config* cfg, unsigned* mc, int* nf, cudaStream_t st, int y0 = 0,
+              int y1 = -1, int ylo = 0, int yhi = -1) {
+    if (y1 < 0) y1 = H;
+    if (yhi < 0) yhi = H - 1;
+    cudaError_t r = launch_fused(u_in, f, u_out, pitch, W, y0, y1, ylo, yhi, batch, bstride, pl->dev.scale,
                                  (float)cfg->epsilon_div, cfg->clamp_nonnegative, mc, nf, st);
     if (r != cudaSuccess) return cuda_err(r, "fused RL iteration launch");
     pl->ctx->launches += 1;
@@ -1182,6 +1185,19 @@ int fdg_solver_pass(fdg_solver* s, int pass, const float* d_in, const float* d_a
         return run_pass(s->adj.get(), g, e, s->ctx->stream);
     }
     return set_err(FDG_EINVAL, "pass must be 1 or 2");
+}
+
+int fdg_solver_iterate(fdg_solver* s, const float* d_f, const float* d_u_in, float* d_u_out, int pitch,
+                       long long image_stride, int y0, int y1, int ylo, int yhi, int iteration) {
+    if (!s || !d_f || !d_u_in || !d_u_out) return set_err(FDG_EINVAL, "null argument");
+    if (d_u_in == d_u_out) return set_err(FDG_EINVAL, "fused iteration: u_in and u_out must differ");
+    if (!use_fused(s->fwd.get())) return set_err(FDG_EINVAL, "solver engine is not fused (see fdg_solver_engine)");
+    if (pitch % 4 || pitch < s->W) return set_err(FDG_EINVAL, "pitch must be a multiple of 4 and >= width");
+    if (ylo > yhi || y0 > y1 || y0 < ylo || y1 - 1 > yhi) return set_err(FDG_EINVAL, "bad row ranges");
+    const int slot = std::min(std::max(iteration, 0), s->ntrace - 1);
+    const long long stride = s->batch > 1 ? image_stride : 0;
+    return run_fused(s->fwd.get(), d_u_in, d_f, d_u_out, pitch, s->W, s->H, s->batch, stride, &s->cfg,
+                     s->maxchange.p + slot, s->nanflag.p + slot, s->ctx->stream, y0, y1, ylo, yhi);
 }
 
 int fdg_solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long image_stride, int iterations) {

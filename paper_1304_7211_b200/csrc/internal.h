@@ -133,9 +133,11 @@ cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float
 bool fused_supported(int mx, int my, int min_dx, int min_dy);
 void set_fused_mode(int v);
 int fused_mode();
-cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int H, int batch,
-                         long long bstride, float scale, float eps, int clamp, unsigned* maxchange, int* nanflag,
-                         cudaStream_t st);
+// Output rows [y0, y1), reads clamped into [ylo, yhi] (the image edges; rows
+// between a shard's core and those edges must hold valid halo rows).
+cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int y0, int y1, int ylo,
+                         int yhi, int batch, long long bstride, float scale, float eps, int clamp,
+                         unsigned* maxchange, int* nanflag, cudaStream_t st);
 // first non-finite / first negative row-major index (~0 if none) -> out[0..1]
 cudaError_t launch_validate(const float* f, int W, int H, int pitch, unsigned long long* out, cudaStream_t st);
 cudaError_t launch_count_inactive(const uint8_t* active, size_t n, unsigned long long* out,

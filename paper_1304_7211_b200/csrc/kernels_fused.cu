@@ -60,7 +60,8 @@ struct FusedArgs {
     const float* f;
     float* u_out;
     int pitch, W, Wp4;
-    int H;  // rows of the image (clamp range [0, H-1])
+    int y0, y1;    // output rows
+    int ylo, yhi;  // readable rows; replicate clamping at these (image) edges
     int band, batch;
     long long bstride;
     float scale, eps;
@@ -178,12 +179,12 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
 
     const int tid = threadIdx.x;
     const int x0 = blockIdx.x * G::CW;
-    const int yb0 = blockIdx.y * a.band;
-    const int yb1 = min(a.H, yb0 + a.band);
+    const int yb0 = a.y0 + blockIdx.y * a.band;
+    const int yb1 = min(a.y1, yb0 + a.band);
     if (yb0 >= yb1) return;
     const long long img = (long long)blockIdx.z * a.bstride;
     const long long pitch = a.pitch;
-    const int qr_lo = max(0, yb0 - RY), qr_hi = min(a.H - 1, yb1 - 1 + RY);
+    const int qr_lo = max(a.ylo, yb0 - RY), qr_hi = min(a.yhi, yb1 - 1 + RY);
     const int nq = qr_hi - qr_lo + 1;  // q rows this band needs
     const int j0 = qr_lo - RY;         // first streamed u row (may be < 0: clamped)
     const int steps = nq + 2 * RY;     // u rows streamed: j0 .. qr_hi + RY
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
             for (int r = 0; r < nr; ++r) {
                 const int j = j0 + st * R + r;
                 bulk_g2s(uring + (size_t)(s * R + r) * G::USEG + udst,
-                         a.u_in + img + (long long)clampi(j, 0, a.H - 1) * pitch + uc0, ubytes, &full[s]);
+                         a.u_in + img + (long long)clampi(j, a.ylo, a.yhi) * pitch + uc0, ubytes, &full[s]);
                 if (j - RY >= qr_lo && j - RY <= qr_hi)
                     l2_prefetch(a.f + img + (long long)(j - RY) * pitch + fc0, fbytes);
             }
@@ -523,10 +524,12 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     const long long cols = (long long)strips * a.batch;
     // one wave of resident CTAs, bands no shorter than 4 MY rows (halo recompute)
     const long long per_wave = std::max(1LL, (long long)sms * occ / cols);
-    const long long ctas_y = std::min(per_wave, std::max(1LL, (long long)a.H / (4 * G::MY)));
-    a.band = (int)((a.H + ctas_y - 1) / ctas_y);
+    const int rows = a.y1 - a.y0;
+    if (rows <= 0) return cudaSuccess;
+    const long long ctas_y = std::min(per_wave, std::max(1LL, (long long)rows / (4 * G::MY)));
+    a.band = (int)((rows + ctas_y - 1) / ctas_y);
     if (const char* e = getenv("FDG_FUSED_BAND")) a.band = std::max(1, atoi(e));
-    dim3 grid(strips, (a.H + a.band - 1) / a.band, a.batch);
+    dim3 grid(strips, (rows + a.band - 1) / a.band, a.batch);
     k_fused<RX, RY, NT, R, S, QR><<<grid, 2 * NT + 32, smem, st>>>(a);
     return cudaGetLastError();
 }
@@ -544,8 +547,8 @@ bool fused_supported(int mx, int my, int min_dx, int min_dy) {
     return g_fused == 1 && mx == 15 && my == 15 && min_dx == -7 && min_dy == -7;
 }
 
-cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int H, int batch,
-                         long long bstride, float scale, float eps, int clamp, unsigned* maxchange, int* nanflag,
+cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int y0, int y1, int ylo,
+                         int yhi, int batch, long long bstride, float scale, float eps, int clamp, unsigned* maxchange, int* nanflag,
                          cudaStream_t st) {
     FusedArgs a;
     a.u_in = u_in;
@@ -554,7 +557,10 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
     a.pitch = pitch;
     a.W = W;
     a.Wp4 = (W + 3) & ~3;
-    a.H = H;
+    a.y0 = y0;
+    a.y1 = y1;
+    a.ylo = ylo;
+    a.yhi = yhi;
     a.batch = batch;
     a.bstride = bstride;
     a.scale = scale;

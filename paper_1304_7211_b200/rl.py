@@ -189,6 +189,13 @@ class RlSolver:
         check(lib().fdg_solver_pass(self.h, which, C.c_void_p(d_in), C.c_void_p(d_aux), C.c_void_p(d_out), pitch,
                                     image_stride, y0, y1, ylo, yhi, iteration))
 
+    def iterate(self, d_f: int, d_u_in: int, d_u_out: int, pitch: int, image_stride: int, y0: int, y1: int,
+                ylo: int, yhi: int, iteration: int):
+        """One whole fused RL iteration on raw device pointers (row strips;
+        engine() must be "fused")."""
+        check(lib().fdg_solver_iterate(self.h, C.c_void_p(d_f), C.c_void_p(d_u_in), C.c_void_p(d_u_out), pitch,
+                                       image_stride, y0, y1, ylo, yhi, iteration))
+
     def trace(self, n: Optional[int] = None):
         """[(max|du|, nan_flag)] per iteration (synchronises)."""
         n = n or max(self.cfg.iterations, 1)

@@ -12,6 +12,10 @@ vertical radius), the device pointer addressing core row 0.  Per iteration:
     exchange(q)
     pass 2        u = max(h* (x) q * u, 0)
 
+With the fused engine (rl_strips_fused) the halo is 2T rows of u and each
+iteration is one exchange + one fused launch that recomputes the q rows
+next to the core.
+
 Replicate clamping happens only at the global first/last row (ylo = 0 on
 rank 0, yhi = core-1 on the last rank); interior strip edges read the
 neighbour's rows, so the sharded result equals the single-GPU one (up to
@@ -91,6 +95,47 @@ class GpuPasses:
         off = s.halo * pitch * 4
         self.solver.pass_(which, src.data_ptr() + off, aux.data_ptr() + off, out.data_ptr() + off, pitch,
                           s.rows * pitch, 0, s.core, s.ylo, s.yhi, k)
+
+
+class GpuFused:
+    """Whole fused RL iterations on the device through libfdgpu
+    (RlSolver.iterate; the solver's engine must be "fused")."""
+
+    def __init__(self, solver):
+        self.solver = solver
+
+    def __call__(self, f: torch.Tensor, u_in: torch.Tensor, u_out: torch.Tensor, s: Strip, k: int):
+        pitch = f.shape[-1]
+        off = s.halo * pitch * 4
+        self.solver.iterate(f.data_ptr() + off, u_in.data_ptr() + off, u_out.data_ptr() + off, pitch,
+                            s.rows * pitch, 0, s.core, s.ylo, s.yhi, k)
+
+
+def fused_halo(psf) -> int:
+    """Halo rows of the fused strip driver: q rows up to the PSF's vertical
+    radius outside the core are recomputed from u, so u needs twice that."""
+    return 2 * psf_halo(psf)
+
+
+def rl_strips_fused(f_local: torch.Tensor, s: Strip, iterations: int, fused: Callable, group=None,
+                    u: Optional[torch.Tensor] = None, u2: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """RL on this rank's strip with one exchange per iteration: the 2T-row
+    u halo (s.halo = fused_halo(psf)), then one fused iteration that
+    recomputes the q rows next to the core ("exchange 14 rows of
+    u once and recompute v and q on the halo rows").  f's halo rows are
+    filled once (the q rows beyond the core read them).  u ping-pongs
+    between two buffers; returns the one holding the result."""
+    if u is None:
+        u = torch.empty_like(f_local)
+    if u2 is None:
+        u2 = torch.empty_like(f_local)
+    exchange(f_local, s, group)
+    u.copy_(f_local)
+    for k in range(iterations):
+        exchange(u, s, group)
+        fused(f_local, u, u2, s, k)
+        u, u2 = u2, u
+    return u
 
 
 def rl_strips(f_local: torch.Tensor, s: Strip, iterations: int, passes: Callable, group=None,

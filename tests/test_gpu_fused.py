@@ -72,3 +72,61 @@ def test_fused_batched_solver():
             ref, _, _ = O.rl_deconvolve(fs[i].astype(np.float64), psf, it, O.BOX2D_SLIDING)
             err = W.max_rel(ud[i, :, :w].cpu().numpy(), ref)
             assert err <= MAX_REL, f"image {i} rep {rep}: {err:.3e}"
+
+
+def test_fused_strips_match_whole_image():
+    """Row strips with a 2T-row u halo (the multi-GPU fused driver), the
+    neighbour exchange emulated by local copies: gathered strips equal the
+    whole-image run (vertical running sums restart per band: fp32 order)."""
+    import torch
+    from paper_1304_7211_b200 import RlSolver
+    from paper_1304_7211_b200 import sharded as S
+    w, h, it, nst = 700, 300, 9, 3
+    f, psf = _input(w, h, 77)
+    dev = torch.device("cuda", 0)
+    pitch = 704
+    rc = RlConfig(iterations=it, op=K.Box2dSliding)
+    solver = RlSolver(psf, rc, w, h)
+    assert solver.engine() == "fused"
+    solver.use_stream(torch.cuda.current_stream(dev).cuda_stream)
+    fw = torch.zeros((h, pitch), device=dev)
+    fw[:, :w] = torch.from_numpy(f)
+    uw = torch.empty_like(fw)
+    solver.run(fw, uw)
+    torch.cuda.synchronize()
+    whole = uw[:, :w].cpu().numpy()
+
+    T = S.fused_halo(psf)
+    strips = [S.strip_of(h, nst, r, T) for r in range(nst)]
+    fs = [S.load_strip(f, s, pitch, device=dev) for s in strips]
+
+    def exchange(bufs):
+        for r in range(nst - 1):
+            a, b, c = bufs[r], bufs[r + 1], strips[r].core
+            b[0:T] = a[c:c + T]
+            a[T + c:2 * T + c] = b[T:2 * T]
+
+    exchange(fs)
+    us = [x.clone() for x in fs]
+    u2 = [torch.empty_like(x) for x in fs]
+    run = S.GpuFused(solver)
+    for k in range(it):
+        exchange(us)
+        for r, s in enumerate(strips):
+            run(fs[r], us[r], u2[r], s, k)
+        us, u2 = u2, us
+    torch.cuda.synchronize()
+    got = np.concatenate([us[r][T:T + s.core, :w].cpu().numpy() for r, s in enumerate(strips)])
+    assert W.max_rel(got, whole) <= 1e-5
+    ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, it, O.BOX2D_SLIDING)
+    assert W.max_rel(got, ref) <= MAX_REL
+
+
+def test_fused_iterate_rejects_non_fused_solver():
+    from paper_1304_7211_b200 import RlSolver
+    from paper_1304_7211_b200._lib import FdgInvalidArgument
+    from paper_1304_7211_b200.psf import makeBoxPsf
+    s = RlSolver(makeBoxPsf(5, 5), RlConfig(iterations=2, op=K.Box2dSliding), 64, 64)
+    assert s.engine() != "fused"
+    with pytest.raises(FdgInvalidArgument):
+        s.iterate(1, 2, 3, 64, 64 * 64, 0, 64, 0, 63, 0)

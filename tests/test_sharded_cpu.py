@@ -35,7 +35,29 @@ class OraclePasses:
         out[T:T + s.core, :w] = torch.from_numpy(res)
 
 
-def _worker(rank, world, port, case, H, W_, it, q):
+class OracleFused:
+    """One whole RL iteration on a strip with a 2T-row u halo (the fused
+    engine's contract): q on rows [-T, core + T) clamped to the readable
+    range, then the adjoint over the core."""
+
+    def __init__(self, psf, op, eps=1e-8):
+        self.psf, self.adj, self.op, self.eps = psf, adjoint(psf), op, eps
+
+    def __call__(self, f, u_in, u_out, s, k):
+        T2, w = s.halo, self.width
+        T = T2 // 2
+        img = u_in[T2 + s.ylo:T2 + s.yhi + 1, :w].numpy()
+        v = O.convolve(img, self.psf, self.op)
+        qlo, qhi = max(s.ylo, -T), min(s.yhi, s.core - 1 + T)
+        vq = v[qlo - s.ylo:qhi - s.ylo + 1]
+        fq = f[T2 + qlo:T2 + qhi + 1, :w].numpy()
+        qb = fq / np.where(vq < self.eps, self.eps, vq)
+        c = O.convolve(qb, self.adj, self.op)[-qlo:-qlo + s.core]
+        uc = u_in[T2:T2 + s.core, :w].numpy()
+        u_out[T2:T2 + s.core, :w] = torch.from_numpy(np.maximum(c * uc, 0.0))
+
+
+def _worker(rank, world, port, case, H, W_, it, q, fused=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -43,11 +65,11 @@ def _worker(rank, world, port, case, H, W_, it, q):
         psf, op = CASES[case]()
         rng = np.random.default_rng(9)
         f = rng.random((H, W_)) + 0.05
-        s = S.strip_of(H, world, rank, S.psf_halo(psf))
+        s = S.strip_of(H, world, rank, S.fused_halo(psf) if fused else S.psf_halo(psf))
         fl = S.load_strip(f, s, W_ + 3, dtype=torch.float64)
-        ex = OraclePasses(psf, op)
+        ex = OracleFused(psf, op) if fused else OraclePasses(psf, op)
         ex.width = W_
-        u = S.rl_strips(fl, s, it, ex)
+        u = S.rl_strips_fused(fl, s, it, ex) if fused else S.rl_strips(fl, s, it, ex)
         full = S.gather_strips(u, s, W_)
         if rank == 0:
             ref, _, _ = O.rl_deconvolve(f, psf, it, op)
@@ -76,6 +98,24 @@ def test_two_rank_strips_equal_single_image(name):
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, 2, port, name, 37, 23, 6, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    err = q.get(timeout=5)
+    assert err < 1e-12, err
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_strips_equal_single_image(world):
+    """The fused strip driver (2T-row u halo, one exchange per iteration,
+    q recomputed next to the core) gives the single-image result."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, "box3x5-box2d", 61, 23, 6, q, True))
+             for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
