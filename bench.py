@@ -406,6 +406,76 @@ def cpu_baseline(cfg):
         return {"value": None, "error": str(e)}
 
 
+def run_thinned(args, cfg, world, rank, local):
+    """Thinned (selective) RL on config 3: the free-running
+    GPU masks (rl.hpp:187-257 with deactivation held off for iterations
+    < 20, reactivation every 10), thresholds calibrated to ~50 % / ~25 %
+    active (profiles/r01_cfg3_thresholds.json).  Headline = effective rate
+    (full-image px x iterations / device loop time); also the active-pixel
+    rate and the unthinned rate of the same input on the same GPU."""
+    import numpy as np
+    import torch
+
+    from paper_1304_7211_b200 import OperatorKind as K, RlConfig, rlDeconvolve, rlDeconvolveSelective
+    from paper_1304_7211_b200 import workloads as W
+    from paper_1304_7211_b200._lib import Context
+
+    if world > 1:
+        if rank == 0:
+            print(json.dumps({"metric": "RL Mpixel*iterations/s", "unavailable":
+                              "thinned config 3 is a single-image replica (SURVEY 8e)"}))
+        return 0
+    torch.cuda.set_device(local)
+    thr = json.load(open(os.path.join(ROOT, "profiles", "r01_cfg3_thresholds.json")))[args.thin]["threshold"]
+    iters = args.iterations or cfg.iterations
+    psf = W.make_psf(cfg.psf)
+    _, f = W.make_input(cfg)
+    ctx = Context(local)
+    rc = RlConfig(iterations=iters, op=K.Naive)
+    for _ in range(args.warmup):
+        rlDeconvolveSelective(f, psf, RlConfig(iterations=min(iters, 25), op=K.Naive), thr, 10, thin_start=20,
+                              ctx=ctx)
+    loops, walls, act = [], [], None
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(args.steps):
+        a = time.perf_counter()
+        r = rlDeconvolveSelective(f, psf, rc, thr, 10, thin_start=20, ctx=ctx)
+        walls.append(time.perf_counter() - a)
+        loops.append(r.trace.totalSeconds())
+        inact = np.array([x.inactiveFraction for x in r.trace.records])
+        act = float(1 - inact[20:].mean()) if iters > 20 else 1.0
+    clocks = sampler.stop()
+    loop_s = statistics.median(loops)
+    un = [rlDeconvolve(f, psf, rc, ctx=ctx).trace.totalSeconds() for _ in range(2)]
+    un_s = min(un)
+    pxit = cfg.width * cfg.height * iters
+    value = pxit / loop_s / 1e6
+    # FLOP actually needed: full 2 x 961 FMA for the unthinned iterations, the
+    # active fraction of it afterwards (SURVEY 8d: 3844 a FLOP per px*it)
+    a_mean = (min(iters, 20) + max(0, iters - 20) * act) / iters
+    tf = DENSE_FLOP_PER_PXIT * a_mean * pxit / loop_s / 1e12
+    line = {"metric": "RL Mpixel*iterations/s (effective, thinned)", "value": value, "unit": "Mpx*it/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": loop_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded BASELINE generator)",
+            "config": {"workload": f"cfg3-{args.thin}", "width": cfg.width, "height": cfg.height, "psf": cfg.psf,
+                       "op": "naive (masked dense)", "iterations": iters, "threshold": thr, "period": 10,
+                       "thin_start": 20, "masks": "free-running on the GPU", "engine": "dense (masked)"},
+            "active_fraction_it21_on": act, "active_px_rate_mpxit": value * a_mean,
+            "unthinned_value": pxit / un_s / 1e6, "speedup_vs_unthinned": un_s / loop_s,
+            "roofline": {"bound": "fp32", "achieved": tf, "peak": FP32_TFLOPS_MEASURED, "unit": "TFLOP/s",
+                         "frac": tf / FP32_TFLOPS_MEASURED, "traffic": None,
+                         "kernel": "k_dense (masked: compacted active 4x4 blocks per 64x64 tile)",
+                         "model": "3844 x active fraction FLOP per px*it (SURVEY 8d)"},
+            "e2e": {"value": pxit / statistics.median(walls) / 1e6, "unit": "Mpx*it/s",
+                    "h2d_bytes_per_step": int(f.nbytes), "d2h_bytes_per_step": int(f.nbytes),
+                    "api": "paper_1304_7211_b200.rlDeconvolveSelective (host buffers)"},
+            "cpu_baseline": None, "gpu_launches": None, "clocks": clocks}
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -415,12 +485,16 @@ def main():
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--iterations", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--thin", default=None, choices=["active50", "active25"],
+                    help="config 3 thinned (selective RL) at the calibrated active fraction")
     args = ap.parse_args()
     from paper_1304_7211_b200 import workloads as W
     cfg = W.CONFIGS[args.config]
     world, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, cfg, world, rank)
+    if args.thin:
+        return run_thinned(args, W.CONFIGS["cfg3"], world, rank, local)
     return run_ours(args, cfg, world, rank, local)
 
 
