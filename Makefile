@@ -36,8 +36,15 @@ oracle: $(ORACLE)
 ref: $(REFLIB)
 cpptests: $(DROPIN)
 
-$(LIB): $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -Xcompiler -fopenmp -shared -o $@ $(CSRC) -lcudart -lgomp
+# one object per source (parallel with make -j); objects live in build/
+OBJS      := $(patsubst $(PKG)/csrc/%,build/%.o,$(CSRC))
+
+build/%.o: $(PKG)/csrc/% $(CHDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -Xcompiler -fopenmp -c -o $@ $<
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -lgomp
 
 $(ORACLE): oracle/psf.c oracle/conv.c oracle/rl.c oracle/oracle.h oracle/plan.h
 	$(HOSTCC) -O3 -std=c11 -D_POSIX_C_SOURCE=200809L -fopenmp -ffp-contract=off -fPIC -shared \
@@ -58,5 +65,6 @@ $(DROPIN): tests/cpp/dropin_test.cpp include/fastdeconv/convolve.hpp include/fas
 
 clean:
 	rm -f $(LIB) $(ORACLE) $(REFLIB) $(DROPIN)
+	rm -rf build
 
 .PHONY: all lib oracle ref cpptests clean

@@ -69,7 +69,8 @@ _lock = threading.Lock()
 
 
 def lib_path() -> str:
-    return os.path.join(HERE, LIB_NAME)
+    # FDG_LIB_PATH: A/B experiments against another in-tree build
+    return os.environ.get("FDG_LIB_PATH") or os.path.join(HERE, LIB_NAME)
 
 
 def lib():

@@ -77,8 +77,10 @@ def thinned(name, g, f, psf, it, thr, label):
 
 def main():
     which = sys.argv[1:] or ["cfg0", "cfg1", "cfg2", "cfg3", "cfg4", "cfg4b"]
-    rows = []
     out = os.path.join(ROOT, "profiles", "r01_full_parity.json")
+    # re-running a subset replaces only those configs' rows
+    old = json.load(open(out)) if os.path.exists(out) else []
+    rows = [r for r in old if r["config"].split("[")[0] not in which]
     for name in which:
         cfg = W.CONFIGS[name]
         psf = W.make_psf(cfg.psf)
