@@ -302,6 +302,7 @@ int build_plan(fdg_ctx* ctx, const HostPsf& psf, int preference, std::unique_ptr
                 for (int y = 0; y < d.mh; ++y)
                     for (int x = 0; x < d.mw; ++x) w[(size_t)y * d.mwp + x] = (float)dense.weights[(size_t)y * d.mw + x];
                 CK(upload(&d.d_dense, w));
+                d.h_dense = w;
             } else {
                 std::vector<Tap> t;
                 for (int y = 0; y < dense.h; ++y)

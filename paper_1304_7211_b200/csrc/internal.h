@@ -64,6 +64,7 @@ struct DevPsf {
     std::vector<int> h_span;     // [2*nrows] xmin,xmax per row (spans engine, host)
     int mw = 0, mh = 0, mwp = 0;  // dense engine: grid, padded width
     float* d_dense = nullptr;     // [mh * mwp]
+    std::vector<float> h_dense;   // host copy (passed as kernel parameters)
 };
 
 enum EpiMode {

@@ -10,7 +10,11 @@
 //          Gaussian).  FP32-FMA-bound (no tensor cores: 961 taps x 2 convs
 //          = 3844 FLOP/px.it).  64x64 output tile, each thread a 4x4 register
 //          block: one shared-memory input row (float4 loads) feeds 4 output
-//          rows x 4 columns x MWP taps; weights are float4 broadcasts.
+//          rows x 4 columns x MWP taps as packed FFMA2, two output columns
+//          per instruction (the tile is also stored shifted by one column, so
+//          every adjacent input pair is an aligned register pair); the
+//          weights come from the kernel parameter space as uniform operands.
+//          Same per-lane fmaf order as scalar FFMA: results are unchanged.
 //          The masked (thinned) variant consumes the per-tile compacted list
 //          of active 4x4 blocks built by k_tile_compact (kernels_mask.cu).
 #include "common.cuh"
@@ -111,19 +115,26 @@ struct DenseArgs {
     int pitch, W;
     int y0, y1, ylo, yhi;
     long long bstride;
-    int min_dx, min_dy, mh, ts;  // ts: tile row stride (floats)
-    const float* wts;            // mh x MWP, zero padded
+    int min_dx, min_dy, mh, ts, th;  // ts: tile row stride (floats), th: tile rows
+    const float* wts;            // mh x MWP, zero padded (device copy)
     const int* tile_blocks;      // masked: per tile up to 256 block ids
     const int* tile_count;
     int tiles_x;
     Epi e;
 };
+// The dense weights travel in the kernel parameter space (constant bank 0,
+// 32 KB limit): the inner loop reads them with a warp-uniform index, which
+// compiles to uniform constant loads (LDCU) feeding FFMA directly -- no
+// shared-memory traffic for the 961 weights.
+struct DenseW {
+    float w[64 * 32];  // mh x MWP row-major, zero padded (8 KB of the 32 KB parameter space)
+};
 
 template <int MWP, int MODE, bool MASKED>
-__global__ void __launch_bounds__(256, 2) k_dense(const DenseArgs a) {
+__global__ void __launch_bounds__(256, 2) k_dense(const DenseArgs a, const __grid_constant__ DenseW wp) {
     extern __shared__ __align__(16) float sm[];
-    float* s_w = sm;                 // mh * MWP
-    float* tile = sm + a.mh * MWP;   // (TD + mh - 1) rows x ts
+    float* tile = sm;                  // (TD + mh - 1) rows x ts
+    float* tile_s = sm + a.th * a.ts;  // the same rows shifted left by one column
     const int tid = threadIdx.x;
     const int tile_id = blockIdx.y * gridDim.x + blockIdx.x;
     int nblk = 256;
@@ -135,54 +146,91 @@ __global__ void __launch_bounds__(256, 2) k_dense(const DenseArgs a) {
     const int oy0 = a.y0 + blockIdx.y * TD;
     const long long img = (long long)blockIdx.z * a.bstride;
     const float* in = a.in + img;
-    for (int i = tid; i < a.mh * MWP; i += 256) s_w[i] = a.wts[i];
     const int th = TD + a.mh - 1;
     const int tw = TD + MWP - 1;
-    for (int i = tid; i < th * tw; i += 256) {
-        const int ty = i / tw, tx = i - ty * tw;
+    // tile column t = image column ox0 + min_dx + t.  Loads go by aligned
+    // float4 chunks of image columns c0 + 4q (c0 = the 16-byte boundary at or
+    // below column ox0 + min_dx), clamped per element only at the image edge.
+    const int cbase = ox0 + a.min_dx;
+    const int c0 = cbase & ~3;  // <= cbase (also for negative cbase)
+    const int sh = cbase - c0;  // tile column of chunk element k: 4 q + k - sh
+    const int nq = (tw + sh + 3) / 4;
+    for (int i = tid; i < th * nq; i += 256) {
+        const int ty = i / nq, q = i - ty * nq;
         const int gy = clampi(oy0 + a.min_dy + ty, a.ylo, a.yhi);
-        const int gx = clampi(ox0 + a.min_dx + tx, 0, a.W - 1);
-        tile[ty * a.ts + tx] = in[(long long)gy * a.pitch + gx];
+        const float* rp = in + (long long)gy * a.pitch;
+        const int c = c0 + 4 * q;
+        float v[4];
+        if (c >= 0 && c + 3 < a.W) {
+            const float4 f4 = __ldg(reinterpret_cast<const float4*>(rp + c));
+            v[0] = f4.x;
+            v[1] = f4.y;
+            v[2] = f4.z;
+            v[3] = f4.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = __ldg(rp + clampi(c + k, 0, a.W - 1));
+        }
+        float* trow = tile + ty * a.ts;
+        float* srow = tile_s + ty * a.ts;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int tx = 4 * q + k - sh;
+            if (tx >= 0 && tx < tw) trow[tx] = v[k];
+            if (tx >= 1 && tx < tw) srow[tx - 1] = v[k];
+        }
     }
     __syncthreads();
     if (tid >= nblk) return;
     int blk = tid;
     if (MASKED) blk = a.tile_blocks[(long long)tile_id * 256 + tid];
     const int bx = blk & 15, by = blk >> 4;
-    float acc[4][4];
+    // packed accumulators: acc[i][0] = outputs (i, 0..1), acc[i][1] = (i, 2..3)
+    float2 acc[4][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
     constexpr int NV = MWP + 4;  // input values per row segment (float4 chunks)
+    constexpr int NP = NV / 2;
     for (int ir = 0; ir < a.mh + 3; ++ir) {
-        float v[NV];
+        // vA[k] = (v[2k], v[2k+1]) and vB[k] = (v[2k+1], v[2k+2]): every
+        // adjacent pair of the window is an aligned register pair, so each
+        // weight (a scalar broadcast operand) feeds two outputs per FFMA2
+        float2 vA[NP], vB[NP];
         const float4* src = reinterpret_cast<const float4*>(tile + (4 * by + ir) * a.ts + 4 * bx);
+        const float4* srs = reinterpret_cast<const float4*>(tile_s + (4 * by + ir) * a.ts + 4 * bx);
 #pragma unroll
         for (int c = 0; c < NV / 4; ++c) {
-            const float4 q = src[c];
-            v[4 * c] = q.x;
-            v[4 * c + 1] = q.y;
-            v[4 * c + 2] = q.z;
-            v[4 * c + 3] = q.w;
+            const float4 q = src[c], qs = srs[c];
+            vA[2 * c] = make_float2(q.x, q.y);
+            vA[2 * c + 1] = make_float2(q.z, q.w);
+            vB[2 * c] = make_float2(qs.x, qs.y);
+            vB[2 * c + 1] = make_float2(qs.z, qs.w);
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int r = ir - i;  // PSF row feeding output row i from input row ir
             if (r < 0 || r >= a.mh) continue;
-            const float4* wr = reinterpret_cast<const float4*>(s_w + r * MWP);
-            float part[4] = {0.f, 0.f, 0.f, 0.f};
+            const float4* wr = reinterpret_cast<const float4*>(wp.w + r * MWP);
+            float2 p01 = make_float2(0.f, 0.f), p23 = make_float2(0.f, 0.f);
 #pragma unroll
             for (int kc = 0; kc < MWP / 4; ++kc) {
                 const float4 w4 = wr[kc];
                 const float wk[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) part[j] = fmaf(wk[e], v[4 * kc + e + j], part[j]);
+                for (int e = 0; e < 4; ++e) {
+                    const int m = 4 * kc + e;  // window offset of output column 0
+                    const float2 ww = make_float2(wk[e], wk[e]);
+                    if ((m & 1) == 0) {
+                        p01 = __ffma2_rn(ww, vA[m / 2], p01);
+                        p23 = __ffma2_rn(ww, vA[m / 2 + 1], p23);
+                    } else {
+                        p01 = __ffma2_rn(ww, vB[m / 2], p01);
+                        p23 = __ffma2_rn(ww, vB[m / 2 + 1], p23);
+                    }
+                }
             }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] += part[j];
+            acc[i][0] = __fadd2_rn(acc[i][0], p01);
+            acc[i][1] = __fadd2_rn(acc[i][1], p23);
         }
     }
     TraceAcc tr;
@@ -196,33 +244,35 @@ __global__ void __launch_bounds__(256, 2) k_dense(const DenseArgs a) {
             if (x >= a.W) continue;
             const long long idx = img + (long long)y * a.pitch + x;
             if (MASKED && !a.e.active[idx]) continue;
-            epilogue<MODE>(a.e, a.out, idx, acc[i][j], tr);
+            const float2 pr = acc[i][j >> 1];
+            epilogue<MODE>(a.e, a.out, idx, (j & 1) ? pr.y : pr.x, tr);
         }
     }
     if (MODE == EPI_UPDATE || MODE == EPI_MUPDATE) trace_flush(a.e, tr);
 }
 
 template <int MWP, int MODE, bool MASKED>
-cudaError_t launch_dense_t(const DenseArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
+cudaError_t launch_dense_t(const DenseArgs& a, const DenseW& w, dim3 grid, size_t smem, cudaStream_t st) {
     cudaError_t err = smem_attr<k_dense<MWP, MODE, MASKED>>();
     if (err != cudaSuccess) return err;
-    k_dense<MWP, MODE, MASKED><<<grid, 256, smem, st>>>(a);
+    k_dense<MWP, MODE, MASKED><<<grid, 256, smem, st>>>(a, w);
     return cudaGetLastError();
 }
 
 template <int MWP>
-cudaError_t dense_mode(const DenseArgs& a, int mode, bool masked, dim3 grid, size_t smem, cudaStream_t st) {
+cudaError_t dense_mode(const DenseArgs& a, const DenseW& w, int mode, bool masked, dim3 grid, size_t smem,
+                       cudaStream_t st) {
     if (!masked) {
         switch (mode) {
-            case EPI_STORE: return launch_dense_t<MWP, EPI_STORE, false>(a, grid, smem, st);
-            case EPI_QUOT: return launch_dense_t<MWP, EPI_QUOT, false>(a, grid, smem, st);
-            case EPI_UPDATE: return launch_dense_t<MWP, EPI_UPDATE, false>(a, grid, smem, st);
+            case EPI_STORE: return launch_dense_t<MWP, EPI_STORE, false>(a, w, grid, smem, st);
+            case EPI_QUOT: return launch_dense_t<MWP, EPI_QUOT, false>(a, w, grid, smem, st);
+            case EPI_UPDATE: return launch_dense_t<MWP, EPI_UPDATE, false>(a, w, grid, smem, st);
         }
     } else {
         switch (mode) {
-            case EPI_STORE: return launch_dense_t<MWP, EPI_STORE, true>(a, grid, smem, st);
-            case EPI_MQUOT: return launch_dense_t<MWP, EPI_MQUOT, true>(a, grid, smem, st);
-            case EPI_MUPDATE: return launch_dense_t<MWP, EPI_MUPDATE, true>(a, grid, smem, st);
+            case EPI_STORE: return launch_dense_t<MWP, EPI_STORE, true>(a, w, grid, smem, st);
+            case EPI_MQUOT: return launch_dense_t<MWP, EPI_MQUOT, true>(a, w, grid, smem, st);
+            case EPI_MUPDATE: return launch_dense_t<MWP, EPI_MUPDATE, true>(a, w, grid, smem, st);
         }
     }
     return cudaErrorInvalidValue;
@@ -302,17 +352,20 @@ cudaError_t launch_dense(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
     const int rows = g.y1 - g.y0;
     if (rows <= 0) return cudaSuccess;
     const int mwp = p.mwp;
-    a.ts = ((TD + mwp - 1 + 4) + 3) & ~3;  // room for the last float4 chunk
-    const int th = TD + p.mh - 1 + 3;
-    const size_t smem = sizeof(float) * ((size_t)p.mh * mwp + (size_t)th * a.ts);
+    a.ts = TD + mwp;       // the last thread's window ends at column TD - 4 + MWP + 3
+    a.th = TD + p.mh - 1;  // rows 4 by + ir, ir < mh + 3
+    const size_t smem = sizeof(float) * 2 * ((size_t)a.th * a.ts);
+    if ((size_t)p.mh * mwp > 64 * 32 || p.h_dense.size() < (size_t)p.mh * mwp) return cudaErrorInvalidValue;
+    DenseW w;
+    for (int i = 0; i < 64 * 32; ++i) w.w[i] = i < p.mh * mwp ? p.h_dense[i] : 0.f;
     dim3 grid((g.W + TD - 1) / TD, (rows + TD - 1) / TD, g.batch);
     a.tiles_x = grid.x;
     const bool masked = d_tile_count != nullptr;
     switch (mwp) {
-        case 4: return dense_mode<4>(a, e.mode, masked, grid, smem, st);
-        case 8: return dense_mode<8>(a, e.mode, masked, grid, smem, st);
-        case 16: return dense_mode<16>(a, e.mode, masked, grid, smem, st);
-        case 32: return dense_mode<32>(a, e.mode, masked, grid, smem, st);
+        case 4: return dense_mode<4>(a, w, e.mode, masked, grid, smem, st);
+        case 8: return dense_mode<8>(a, w, e.mode, masked, grid, smem, st);
+        case 16: return dense_mode<16>(a, w, e.mode, masked, grid, smem, st);
+        case 32: return dense_mode<32>(a, w, e.mode, masked, grid, smem, st);
     }
     return cudaErrorInvalidValue;
 }
