@@ -95,6 +95,9 @@ int fdg_device_available(void);
 /* Process-wide engine options (no reference counterpart; tuning/testing):
  *   "fused": 1 = run each RL iteration of the centred 15x15 box as one fused
  *            pass (kernels_fused.cu, default), 0 = two fused-epilogue passes.
+ *   "spans": GenericBox span-table kernels (kernels_spans.cu): 0 = by size
+ *            (tile kernel up to 4.5 Mpx per launch, default), 1 = tile
+ *            kernel, 2 = marching kernel.
  * Returns the previous value, or -1 for an unknown name. */
 int fdg_set_option(const char* name, int value);
 

@@ -617,6 +617,11 @@ int fdg_set_option(const char* name, int value) {
         set_fused_mode(value);
         return prev;
     }
+    if (name && std::strcmp(name, "spans") == 0) {  // 0 auto, 1 tile kernel, 2 marching kernel
+        const int prev = spans_mode();
+        set_spans_mode(value);
+        return prev;
+    }
     return -1;
 }
 

@@ -107,6 +107,9 @@ cudaError_t launch_dense(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
                          const int* d_tile_blocks, const int* d_tile_count);
 cudaError_t launch_spans(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st);
 bool spans_supported(const DevPsf& p);
+// spans kernel choice: 0 = by image size (tile <= 4.5 Mpx per launch), 1 = tile, 2 = marching
+void set_spans_mode(int v);
+int spans_mode();
 bool dense_supported(const DevPsf& p);
 
 // compaction (kernels_mask.cu)

@@ -611,11 +611,12 @@ cudaError_t launch_shape(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
     a.nanflag = e.nanflag;
     static const int nt_env = env_int("FDG_SPANS_NT");
     static const int g_env = env_int("FDG_SPANS_G");
-    static const int tile_env = env_int("FDG_SPANS_TILE");  // 1: tile, 2: marching (A/B)
     // Small images (<= 4.5 Mpx per launch): the tile kernel -- the marching
-    // grid cannot fill the SMs (profiles/r01_spans_notes.md); larger ones march.
+    // grid cannot fill the SMs (profiles/r01_spans_notes.md); larger ones
+    // march.  fdg_set_option("spans", 1 | 2) forces one (tests, A/B).
     const long long px = (long long)g.W * (g.y1 - g.y0) * g.batch;
-    const bool tile = tile_env ? tile_env == 1 : px <= 4608ll * 1024;
+    const int mode = spans_mode();
+    const bool tile = mode ? mode == 1 : px <= 4608ll * 1024;
     if (tile) {
         if (SH::NR > 16) return launch_tile<SH, 8, 8, false>(a, g, e, st);  // disc: 128 x 64 tiles
         return launch_tile<SH, 4, 8, true>(a, g, e, st);                    // oblique: 128 x 32, aux prefetch
@@ -626,7 +627,12 @@ cudaError_t launch_shape(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
     return narrow ? launch_nt<SH, 64, 1>(a, g, e, st) : launch_nt<SH, 128, 1>(a, g, e, st);
 }
 
+int g_spans_mode = env_int("FDG_SPANS_TILE");
+
 }  // namespace
+
+void set_spans_mode(int v) { g_spans_mode = v; }
+int spans_mode() { return g_spans_mode; }
 
 bool spans_supported(const DevPsf& p) {
     if (getenv("FDG_NO_SPANS")) return false;

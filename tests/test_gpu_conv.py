@@ -137,3 +137,22 @@ def test_engine_selection():
     assert ConvPlan(W.disc_r10(), K.GenericBox).engine() == "spans"
     assert ConvPlan(W.oblique_line(), K.GenericBox).engine() == "spans"
     assert ConvPlan(makeDiscPsf(9), K.GenericBox).engine() == "taps"
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("name", ["disc10", "oblique"])
+def test_spans_kernels_both_paths(mode, name):
+    """The span-table engine has a tile kernel (small images) and a marching
+    kernel (large ones); force each on awkward sizes (width not a multiple of
+    4, narrower than the halo, one row, several strips / bands)."""
+    from paper_1304_7211_b200._lib import lib
+    psf = psf_zoo()[name]
+    prev = lib().fdg_set_option(b"spans", mode)
+    try:
+        rng = np.random.default_rng(11 + mode)
+        for h, w in [(1, 7), (3, 130), (70, 9), (131, 259), (300, 513), (517, 1030)]:
+            img = rng.random((h, w)).astype(np.float32).astype(np.float64)
+            assert ConvPlan(psf, K.GenericBox).engine() == "spans"
+            close(convolve(img, psf, K.GenericBox), O.convolve(img, psf, O.GENERIC_BOX))
+    finally:
+        lib().fdg_set_option(b"spans", prev)

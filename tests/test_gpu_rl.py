@@ -205,3 +205,15 @@ def test_device_solver_graph_replay_matches_host_api():
     assert W.max_rel(u2.cpu().numpy(), host) <= 1e-5
     mc = [m for m, _ in solver.trace(25)]
     assert all(m > 0 for m in mc)
+
+
+@pytest.mark.parametrize("name,w,h", [("cfg1", 640, 480), ("cfg2", 512, 512)])
+def test_spans_marching_kernel_rl(name, w, h):
+    """RL on the marching span kernel (the default for images > 4.5 Mpx),
+    forced on a reduced config; the tile kernel runs these sizes by default."""
+    from paper_1304_7211_b200._lib import lib
+    prev = lib().fdg_set_option(b"spans", 2)
+    try:
+        run_config(name, w, h, iterations=60)
+    finally:
+        lib().fdg_set_option(b"spans", prev)
