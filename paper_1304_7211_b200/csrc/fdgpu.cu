@@ -83,6 +83,10 @@ struct fdg_ctx {
     DevBuf<unsigned> tr_max;
     DevBuf<int> tr_nan;
     DevBuf<unsigned long long> tr_inact, first_bad;
+    // rlDeconvolve on host buffers keeps the last call's solver (plans + the
+    // captured CUDA graph of the iteration loop) keyed by PSF, config and size
+    fdg_solver* rl_solver = nullptr;
+    std::string rl_key;
 };
 
 struct fdg_plan {
@@ -653,6 +657,7 @@ int fdg_ctx_create(int device, fdg_ctx** out) {
 void fdg_ctx_destroy(fdg_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    fdg_solver_destroy(ctx->rl_solver);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -863,6 +868,33 @@ int fdg_conv_apply_masked(fdg_plan* pl, const float* in, int W, int H, const uin
     return FDG_OK;
 }
 
+// Cache key of a host-buffer RL call: every field of the PSF descriptor, the
+// config and the image size (the solver's plans and graph depend on nothing else).
+static std::string rl_cache_key(const fdg_psf_desc* d, const fdg_rl_config* c, int W, int H) {
+    std::string k;
+    auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
+    const int hdr[9] = {d ? d->repr : -1, d ? d->width : 0, d ? d->height : 0, d ? d->anchor_x : 0,
+                        d ? d->anchor_y : 0, d ? d->n_rows : 0, d ? d->n_taps : 0, W, H};
+    put(hdr, sizeof hdr);
+    put(&c->iterations, sizeof c->iterations);
+    put(&c->op, sizeof c->op);
+    put(&c->epsilon_div, sizeof c->epsilon_div);
+    put(&c->clamp_nonnegative, sizeof c->clamp_nonnegative);
+    if (!d) return k;
+    if (d->weights && d->width > 0 && d->height > 0) put(d->weights, sizeof(double) * d->width * d->height);
+    if (d->n_rows > 0) {
+        if (d->row_dy) put(d->row_dy, sizeof(int) * d->n_rows);
+        if (d->row_xmin) put(d->row_xmin, sizeof(int) * d->n_rows);
+        if (d->row_xmax) put(d->row_xmax, sizeof(int) * d->n_rows);
+    }
+    if (d->n_taps > 0) {
+        if (d->tap_dx) put(d->tap_dx, sizeof(int) * d->n_taps);
+        if (d->tap_dy) put(d->tap_dy, sizeof(int) * d->n_taps);
+        if (d->tap_w) put(d->tap_w, sizeof(double) * d->n_taps);
+    }
+    return k;
+}
+
 int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, const float* f, int W,
                       int H, float* u_out, fdg_rl_record* trace) {
     PhaseTimer pt;
@@ -873,8 +905,25 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
         return check_device(ctx);
     }
     if ((st = check_device(ctx))) return st;
+    // Repeated calls with the same PSF / config / size replay the solver's
+    // captured graph (one cudaGraphLaunch for the whole iteration loop)
+    static const bool no_cache = getenv("FDG_NO_RL_CACHE") != nullptr;
+    fdg_solver* sv = nullptr;
+    if (!no_cache && cfg->iterations >= 1) {
+        std::string key = rl_cache_key(desc, cfg, W, H);
+        if (!ctx->rl_solver || ctx->rl_key != key) {
+            fdg_solver_destroy(ctx->rl_solver);
+            ctx->rl_solver = nullptr;
+            ctx->rl_key.clear();
+            fdg_solver* ns = nullptr;
+            if ((st = fdg_solver_create(ctx, desc, cfg, W, H, 1, &ns))) return st;
+            ctx->rl_solver = ns;
+            ctx->rl_key = std::move(key);
+        }
+        sv = ctx->rl_solver;
+    }
     std::unique_ptr<fdg_plan> fwd, adj;
-    if ((st = make_rl_plans(ctx, desc, cfg->op, &fwd, &adj))) return st;
+    if (!sv && (st = make_rl_plans(ctx, desc, cfg->op, &fwd, &adj))) return st;
     pt.mark("plans");
     const int iters = cfg->iterations;
     const int pitch = pitch_for(W);
@@ -892,6 +941,34 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     if ((st = h2d(df, pitch, f, W, H, s))) return st;
     if ((st = validate_device(ctx, df, W, H, pitch, "rlDeconvolve"))) return st;
     pt.mark("h2d+validate");
+    if (sv) {
+        EventPool ev;
+        if (trace) {
+            CK(ev.make(2));
+            CK(cudaEventRecord(ev.ev[0], s));
+        }
+        if ((st = fdg_solver_reset_trace(sv))) return st;
+        if ((st = fdg_solver_run(sv, df, du, pitch, 0, iters))) return st;
+        if (trace) CK(cudaEventRecord(ev.ev[1], s));
+        prefault(u_out, (size_t)W * H * sizeof(float));
+        if (pt.on) {
+            CK(cudaStreamSynchronize(s));
+            pt.mark("iterate(graph)");
+        }
+        if ((st = d2h(u_out, du, pitch, W, H, s))) return st;
+        std::vector<fdg_rl_record> rec(iters);
+        if ((st = fdg_solver_trace(sv, rec.data(), iters))) return st;  // synchronises the stream
+        pt.mark("d2h");
+        float ms = 0.f;
+        if (trace) cudaEventElapsedTime(&ms, ev.ev[0], ev.ev[1]);
+        for (int k = 0; k < iters; ++k) {
+            if (rec[k].inactive_fraction != 0.0)  // the solver trace's NaN slot
+                return set_err(FDG_ENAN, "rlDeconvolve: NaN in iterate at iteration " + std::to_string(k + 1));
+            // one graph for the whole loop: per-iteration seconds = run time / iterations
+            if (trace) trace[k] = {k + 1, 0.0, rec[k].max_abs_change, ms * 1e-3 / iters};
+        }
+        return FDG_OK;
+    }
     CK(cudaMemsetAsync(mc, 0, sizeof(unsigned) * (iters + 1), s));
     CK(cudaMemsetAsync(nf, 0, sizeof(int) * (iters + 1), s));
     CK(cudaMemcpyAsync(du, df, n * sizeof(float), cudaMemcpyDeviceToDevice, s));

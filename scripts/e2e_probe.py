@@ -10,7 +10,7 @@ from paper_1304_7211_b200._lib import Context
 cfg = W.CONFIGS["cfg4"]
 psf = W.make_psf(cfg.psf)
 dev = torch.device("cuda", 0)
-f = bench.make_input_gpu(cfg, psf, dev)
+f = bench.make_input_gpu(cfg, psf, dev).cpu().numpy()
 ctx = Context(0)
 rc = RlConfig(iterations=100, op=K.Box2dSliding)
 fp = torch.from_numpy(f).pin_memory().numpy()
