@@ -7,7 +7,8 @@ model lives in :mod:`.psf`, operators in :mod:`.convolve`, the RL drivers in
 ``FdgError`` when the library or a CUDA device is missing.
 """
 from .psf import (DensePsf, UniformConvexPsf, SparsePsf, makeLinePsf, makeBoxPsf, makeDiscPsf,
-                  makeDiagonalPsf, adjoint, taps_of)
+                  makeDiagonalPsf, adjoint, taps_of, toSparse, parseSparsePsf, formatSparsePsf, parsePsfSpec)
+from .pgm import PgmParseError, readPgm, writePgm, readPgmFile, writePgmFile, snrDb
 from .convolve import (OperatorKind, operatorName, operatorKindFromName, supportsMasking,
                        operatorAcceptsPsf, dispatch, ConvCounters, ConvPlan, convolve, maskedConvolve)
 from .rl import (RlConfig, RlIterationRecord, RlTrace, RlResult, rlDeconvolve, rlDeconvolveSelective,

@@ -11,6 +11,7 @@ validates, normalises and marshals.
 from __future__ import annotations
 
 import math
+import re
 from typing import Iterable, List, Sequence, Tuple
 
 import numpy as np
@@ -181,3 +182,81 @@ def adjoint(psf):
     if isinstance(psf, UniformConvexPsf):
         return UniformConvexPsf([(-dy, -hi, -lo) for dy, lo, hi in reversed(psf.rows)])
     return SparsePsf([(-dx, -dy, w) for dx, dy, w in psf._raw])
+
+
+# ------------------------------------------------- sparse text format (CLI)
+def parseSparsePsf(text: str) -> SparsePsf:
+    """One "dx dy weight" triple per line, '#' comment and blank lines ignored,
+    weights renormalised on load (psf.hpp:231-262).  Errors name the line."""
+    taps, seen = [], set()
+    for line_no, line in enumerate(text.split("\n"), start=1):
+        if line.endswith("\r"):
+            line = line[:-1]
+        s = line.lstrip(" \t")
+        if not s or s.startswith("#"):
+            continue
+        parts = line.split()
+        try:
+            if len(parts) != 3:
+                raise ValueError
+            dx, dy, w = int(parts[0]), int(parts[1]), float(parts[2])
+        except ValueError:
+            raise RuntimeError(f"sparse PSF: line {line_no}: expected 'dx dy weight'") from None
+        if not (w > 0.0) or not math.isfinite(w):
+            raise RuntimeError(f"sparse PSF: line {line_no}: weight must be positive")
+        if (dx, dy) in seen:
+            raise RuntimeError(f"sparse PSF: line {line_no}: duplicate tap ({dx}, {dy})")
+        seen.add((dx, dy))
+        taps.append((dx, dy, w))
+    if not taps:
+        raise RuntimeError("sparse PSF: no taps found")
+    return SparsePsf(taps)
+
+
+def formatSparsePsf(psf: SparsePsf) -> str:
+    """Inverse of parseSparsePsf, 17 significant digits (psf.hpp:264-271)."""
+    out = ["# dx dy weight"]
+    for dx, dy, w in psf.taps:
+        out.append(f"{dx} {dy} {w:.17g}")
+    return "\n".join(out) + "\n"
+
+
+def toSparse(psf) -> SparsePsf:
+    """Non-zero taps of any representation, in the reference's toSparse order."""
+    return SparsePsf([(dx, dy, w) for dx, dy, w in taps_of(psf) if w != 0.0])
+
+
+def parsePsfSpec(spec: str):
+    """CLI PSF grammar line:<M> | box:<MX>x<MY> | disc:<D> | diag:<M> |
+    file:<path> (fastdeconv_cli.cpp:16-58), same error messages."""
+    if ":" not in spec:
+        raise RuntimeError(f"bad PSF spec '{spec}' (expected line:<M>, box:<MX>x<MY>, disc:<D>, diag:<M>, "
+                           "or file:<path>)")
+    kind, arg = spec.split(":", 1)
+
+    def size(s: str) -> int:  # std::stoi consuming the whole argument, value >= 1
+        ok = re.fullmatch(r"[ \t\n\v\f\r]*[+-]?[0-9]+", s) is not None
+        v = int(s) if ok else 0
+        if v < 1 or v > 2**31 - 1:
+            raise RuntimeError(f"bad PSF size '{s}' in spec '{spec}'")
+        return v
+
+    if kind == "line":
+        return makeLinePsf(size(arg))
+    if kind == "disc":
+        return makeDiscPsf(size(arg))
+    if kind == "diag":
+        return makeDiagonalPsf(size(arg))
+    if kind == "box":
+        if "x" not in arg:
+            raise RuntimeError(f"bad box spec '{spec}' (expected box:<MX>x<MY>)")
+        a, b = arg.split("x", 1)
+        return makeBoxPsf(size(a), size(b))
+    if kind == "file":
+        try:
+            with open(arg) as fh:
+                text = fh.read()
+        except OSError:
+            raise RuntimeError(f"cannot open PSF file: {arg}") from None
+        return parseSparsePsf(text)
+    raise RuntimeError(f"unknown PSF kind '{kind}' in spec '{spec}'")
