@@ -130,3 +130,61 @@ def test_fused_iterate_rejects_non_fused_solver():
     assert s.engine() != "fused"
     with pytest.raises(FdgInvalidArgument):
         s.iterate(1, 2, 3, 64, 64 * 64, 0, 64, 0, 63, 0)
+
+
+@pytest.mark.parametrize("psf_name,op,spans_mode", [("disc10", K.GenericBox, 1), ("disc10", K.GenericBox, 2),
+                                                    ("oblique21", K.GenericBox, 0), ("gauss31", K.Naive, 0),
+                                                    ("line31", K.Box1dSliding, 0), ("box15x15", K.Box2dSliding, 0)])
+def test_two_pass_strips_match_whole_image(psf_name, op, spans_mode):
+    """The multi-GPU two-pass strip driver (sharded.rl_strips + GpuPasses:
+    T-row halos of u and q, row ranges and clamp ranges per strip) on one
+    device, the exchange emulated by local copies, for every engine the
+    strips can hit: gathered strips equal the whole-image run."""
+    import torch
+    from paper_1304_7211_b200 import RlSolver
+    from paper_1304_7211_b200 import sharded as S
+    from paper_1304_7211_b200._lib import lib
+    w, h, it, nst = 333, 260, 6, 3
+    psf = W.make_psf(psf_name)
+    rng = np.random.default_rng(5)
+    f = (rng.random((h, w)) * 0.9 + 0.1).astype(np.float32)
+    dev = torch.device("cuda", 0)
+    pitch = 336
+    prev_f = lib().fdg_set_option(b"fused", 0)  # the box goes through its two-pass kernels here
+    prev_s = lib().fdg_set_option(b"spans", spans_mode)
+    try:
+        solver = RlSolver(psf, RlConfig(iterations=it, op=op), w, h)
+        solver.use_stream(torch.cuda.current_stream(dev).cuda_stream)
+        fw = torch.zeros((h, pitch), device=dev)
+        fw[:, :w] = torch.from_numpy(f)
+        uw = torch.empty_like(fw)
+        solver.run(fw, uw)
+        torch.cuda.synchronize()
+        whole = uw[:, :w].cpu().numpy()
+
+        T = S.psf_halo(psf)
+        strips = [S.strip_of(h, nst, r, T) for r in range(nst)]
+        fs = [S.load_strip(f, s, pitch, device=dev) for s in strips]
+        us = [x.clone() for x in fs]
+        qs = [torch.zeros_like(x) for x in fs]
+
+        def exchange(bufs):
+            for r in range(nst - 1):
+                a, b, c = bufs[r], bufs[r + 1], strips[r].core
+                b[0:T] = a[c:c + T]
+                a[T + c:2 * T + c] = b[T:2 * T]
+
+        run = S.GpuPasses(solver)
+        for k in range(it):
+            exchange(us)
+            for r, s in enumerate(strips):
+                run(1, us[r], fs[r], qs[r], s, k)
+            exchange(qs)
+            for r, s in enumerate(strips):
+                run(2, qs[r], us[r], us[r], s, k)
+        torch.cuda.synchronize()
+    finally:
+        lib().fdg_set_option(b"fused", prev_f)
+        lib().fdg_set_option(b"spans", prev_s)
+    got = np.concatenate([us[r][T:T + s.core, :w].cpu().numpy() for r, s in enumerate(strips)])
+    assert W.max_rel(got, whole) <= 1e-5  # same engine per strip; fp32 order differs only for box running sums
