@@ -172,19 +172,45 @@ cudaError_t launch_quot_const(const float* f, float* q, int W, int H, int pitch,
 
 namespace fdg {
 namespace {
+// first non-finite / first negative row-major index: float4 per thread
+// (rows are 16-byte aligned, pitch % 4 == 0), one integer division per 4 px
 __global__ void k_validate(const float* f, int W, int H, int pitch, unsigned long long* out) {
-    unsigned bad_nf = ~0u, bad_neg = ~0u;  // row-major indices (images < 2^32 px)
-    const long long n = (long long)W * H;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const float v = f[(i / W) * (long long)pitch + (i % W)];
-        if (!isfinite(v)) bad_nf = min(bad_nf, (unsigned)i);
-        else if (v < 0.f) bad_neg = min(bad_neg, (unsigned)i);
+    unsigned long long bad_nf = ~0ull, bad_neg = ~0ull;
+    const long long nq = (W + 3) / 4;
+    const long long n = nq * H;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+        const long long y = t / nq;
+        const int x = 4 * (int)(t - y * nq);
+        const float* row = f + y * pitch;
+        float v[4];
+        if (x + 3 < W) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(row + x));
+            v[0] = q.x;
+            v[1] = q.y;
+            v[2] = q.z;
+            v[3] = q.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = x + e < W ? row[x + e] : 0.f;
+        }
+        const unsigned long long base = (unsigned long long)y * W + x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (!isfinite(v[e])) bad_nf = min(bad_nf, base + e);
+            else if (v[e] < 0.f) bad_neg = min(bad_neg, base + e);
+        }
     }
-    bad_nf = __reduce_min_sync(0xffffffffu, bad_nf);
-    bad_neg = __reduce_min_sync(0xffffffffu, bad_neg);
+    // warp minimum of 64-bit values: two 32-bit passes
+    auto wmin = [](unsigned long long v) {
+        const unsigned hi = __reduce_min_sync(0xffffffffu, (unsigned)(v >> 32));
+        const unsigned lo = __reduce_min_sync(0xffffffffu, (unsigned)(v >> 32) == hi ? (unsigned)v : ~0u);
+        return ((unsigned long long)hi << 32) | lo;
+    };
+    bad_nf = wmin(bad_nf);
+    bad_neg = wmin(bad_neg);
     if ((threadIdx.x & 31) == 0) {
-        if (bad_nf != ~0u) atomicMin(&out[0], (unsigned long long)bad_nf);
-        if (bad_neg != ~0u) atomicMin(&out[1], (unsigned long long)bad_neg);
+        if (bad_nf != ~0ull) atomicMin(&out[0], bad_nf);
+        if (bad_neg != ~0ull) atomicMin(&out[1], bad_neg);
     }
 }
 __global__ void k_fill_u64(unsigned long long* p, int n) {

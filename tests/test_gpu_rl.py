@@ -217,3 +217,24 @@ def test_spans_marching_kernel_rl(name, w, h):
         run_config(name, w, h, iterations=60)
     finally:
         lib().fdg_set_option(b"spans", prev)
+
+
+@pytest.mark.parametrize("w,h", [(1, 1), (5, 3), (7, 9), (130, 67), (1027, 515)])
+def test_validation_first_bad_pixel_order(w, h):
+    """rl.hpp:78-83: the first offending pixel in row-major order decides the
+    message (non-finite before negative at the same pixel); the device scan
+    runs float4 chunks with a scalar tail, so probe heads, tails and both
+    orders."""
+    rng = np.random.default_rng(w * 1000 + h)
+    for _ in range(6):
+        f = np.ones((h, w), np.float32)
+        i_neg, i_nan = rng.integers(0, w * h, 2)
+        f.flat[i_neg] = -1.0
+        f.flat[i_nan] = np.inf if rng.random() < 0.5 else np.nan
+        msg = "non-finite" if i_nan <= i_neg else "nonnegative"
+        with pytest.raises(ValueError, match=msg):
+            rlDeconvolve(f, makeBoxPsf(1, 1), RlConfig(iterations=1))
+    f = np.ones((h, w), np.float32)
+    f.flat[w * h - 1] = -0.5  # the very last pixel (tail chunk)
+    with pytest.raises(ValueError, match="nonnegative"):
+        rlDeconvolve(f, makeBoxPsf(1, 1), RlConfig(iterations=1))
