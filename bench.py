@@ -438,6 +438,7 @@ def run_thinned(args, cfg, world, rank, local):
     loops, walls, act = [], [], None
     sampler = ClockSampler(local)
     sampler.start()
+    launches0 = ctx.launch_count()
     for _ in range(args.steps):
         a = time.perf_counter()
         r = rlDeconvolveSelective(f, psf, rc, thr, 10, thin_start=20, ctx=ctx)
@@ -446,6 +447,7 @@ def run_thinned(args, cfg, world, rank, local):
         inact = np.array([x.inactiveFraction for x in r.trace.records])
         act = float(1 - inact[20:].mean()) if iters > 20 else 1.0
     clocks = sampler.stop()
+    launches = ctx.launch_count() - launches0
     loop_s = statistics.median(loops)
     un = [rlDeconvolve(f, psf, rc, ctx=ctx).trace.totalSeconds() for _ in range(2)]
     un_s = min(un)
@@ -471,7 +473,7 @@ def run_thinned(args, cfg, world, rank, local):
             "e2e": {"value": pxit / statistics.median(walls) / 1e6, "unit": "Mpx*it/s",
                     "h2d_bytes_per_step": int(f.nbytes), "d2h_bytes_per_step": int(f.nbytes),
                     "api": "paper_1304_7211_b200.rlDeconvolveSelective (host buffers)"},
-            "cpu_baseline": None, "gpu_launches": None, "clocks": clocks}
+            "cpu_baseline": None, "gpu_launches": launches, "clocks": clocks}
     print(json.dumps(line))
     return 0
 
