@@ -63,6 +63,7 @@ struct FusedArgs {
     int y0, y1;    // output rows
     int ylo, yhi;  // readable rows; replicate clamping at these (image) edges
     int band, batch;
+    int lin_len, strips;  // lin_len > 0: work-balanced row ranges over the strips (batch 1)
     long long bstride;
     float scale, eps;
     int clamp;
@@ -178,321 +179,351 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     float4* v2 = v1 + MY * NT;                                    // MY x NT
 
     const int tid = threadIdx.x;
-    const int x0 = blockIdx.x * G::CW;
-    const int yb0 = a.y0 + blockIdx.y * a.band;
-    const int yb1 = min(a.y1, yb0 + a.band);
-    if (yb0 >= yb1) return;
     const long long img = (long long)blockIdx.z * a.bstride;
     const long long pitch = a.pitch;
-    const int qr_lo = max(a.ylo, yb0 - RY), qr_hi = min(a.yhi, yb1 - 1 + RY);
-    const int nq = qr_hi - qr_lo + 1;  // q rows this band needs
-    const int j0 = qr_lo - RY;         // first streamed u row (may be < 0: clamped)
-    const int steps = nq + 2 * RY;     // u rows streamed: j0 .. qr_hi + RY
-    const int useg0 = x0 - 2 * G::HX;  // image column of u-segment index 0
-    // the u segment reaches outside the image: replicate columns 0 / W-1 there
-    const bool edge_cta = useg0 < 0 || x0 + G::CW + 2 * G::HX > a.W;
+    // one column strip x0, output rows [yb0, yb1): fresh barriers, every role
+    // runs its pipeline to the end of the segment
+    auto run_segment = [&](const int x0, const int yb0, const int yb1) {
+        const int qr_lo = max(a.ylo, yb0 - RY), qr_hi = min(a.yhi, yb1 - 1 + RY);
+        const int nq = qr_hi - qr_lo + 1;  // q rows this band needs
+        const int j0 = qr_lo - RY;         // first streamed u row (may be < 0: clamped)
+        const int steps = nq + 2 * RY;     // u rows streamed: j0 .. qr_hi + RY
+        const int useg0 = x0 - 2 * G::HX;  // image column of u-segment index 0
+        // the u segment reaches outside the image: replicate columns 0 / W-1 there
+        const bool edge_cta = useg0 < 0 || x0 + G::CW + 2 * G::HX > a.W;
 
-    if (tid == 0) {
-        for (int s = 0; s < SS; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NT);  // every A thread arrives
-            mbar_init(&ready[s], 32);
-        }
-        for (int r = 0; r < QR; ++r) {
-            mbar_init(&qfull[r], NT);   // A threads publish a q row
-            mbar_init(&qempty[r], NT);  // B threads are done reading it
-        }
-        mbar_fence_init();
-    }
-    __syncthreads();
-
-    if (tid >= 2 * NT) {  // ------------------------------------ producer warp
-        const int lane = tid - 2 * NT;
-        const int nst = (steps + R - 1) / R;
-        const int uc0 = max(0, useg0), uc1 = min(a.Wp4, x0 + G::CW + 2 * G::HX);
-        const unsigned ubytes = (unsigned)(uc1 - uc0) * 4u;
-        const int udst = uc0 - useg0;
-        const int fc0 = max(0, x0 - G::HX), fc1 = min(a.Wp4, x0 + G::CW + G::HX);
-        const unsigned fbytes = (unsigned)(fc1 - fc0) * 4u;
-        auto issue = [&](int st) {
-            const int s = st % SS;
-            if (st >= SS) mbar_wait_sleep(&empty[s], ((st / SS) - 1) & 1, 200);
-            const int nr = min(R, steps - st * R);
-            mbar_arrive_expect_tx(&full[s], ubytes * nr);
-            for (int r = 0; r < nr; ++r) {
-                const int j = j0 + st * R + r;
-                bulk_g2s(uring + (size_t)(s * R + r) * G::USEG + udst,
-                         a.u_in + img + (long long)clampi(j, a.ylo, a.yhi) * pitch + uc0, ubytes, &full[s]);
-                if (j - RY >= qr_lo && j - RY <= qr_hi)
-                    l2_prefetch(a.f + img + (long long)(j - RY) * pitch + fc0, fbytes);
+        if (tid == 0) {
+            for (int s = 0; s < SS; ++s) {
+                mbar_init(&full[s], 1);
+                mbar_init(&empty[s], NT);  // every A thread arrives
+                mbar_init(&ready[s], 32);
             }
-        };
-        if (!edge_cta) {
-            if (lane == 0)
-                for (int st = 0; st < nst; ++st) issue(st);
+            for (int r = 0; r < QR; ++r) {
+                mbar_init(&qfull[r], NT);   // A threads publish a q row
+                mbar_init(&qempty[r], NT);  // B threads are done reading it
+            }
+            mbar_fence_init();
+        }
+        __syncthreads();
+
+        if (tid >= 2 * NT) {  // ------------------------------------ producer warp
+            const int lane = tid - 2 * NT;
+            const int nst = (steps + R - 1) / R;
+            const int uc0 = max(0, useg0), uc1 = min(a.Wp4, x0 + G::CW + 2 * G::HX);
+            const unsigned ubytes = (unsigned)(uc1 - uc0) * 4u;
+            const int udst = uc0 - useg0;
+            const int fc0 = max(0, x0 - G::HX), fc1 = min(a.Wp4, x0 + G::CW + G::HX);
+            const unsigned fbytes = (unsigned)(fc1 - fc0) * 4u;
+            auto issue = [&](int st) {
+                const int s = st % SS;
+                if (st >= SS) mbar_wait_sleep(&empty[s], ((st / SS) - 1) & 1, 200);
+                const int nr = min(R, steps - st * R);
+                mbar_arrive_expect_tx(&full[s], ubytes * nr);
+                for (int r = 0; r < nr; ++r) {
+                    const int j = j0 + st * R + r;
+                    bulk_g2s(uring + (size_t)(s * R + r) * G::USEG + udst,
+                             a.u_in + img + (long long)clampi(j, a.ylo, a.yhi) * pitch + uc0, ubytes, &full[s]);
+                    if (j - RY >= qr_lo && j - RY <= qr_hi)
+                        l2_prefetch(a.f + img + (long long)(j - RY) * pitch + fc0, fbytes);
+                }
+            };
+            if (!edge_cta) {
+                if (lane == 0)
+                    for (int st = 0; st < nst; ++st) issue(st);
+                return;
+            }
+            const int lo_end = max(0, -useg0);       // segment indices [0, lo_end) are left of column 0
+            const int hi_beg = max(0, a.W - useg0);  // [hi_beg, UW) are right of column W-1
+            const int i0c = lo_end, iWc = a.W - 1 - useg0;
+            for (int st = 0; st < nst + LAG; ++st) {
+                if (st < nst && lane == 0) issue(st);
+                const int sd = st - LAG;
+                if (sd >= 0 && sd < nst) {
+                    const int s = sd % SS;
+                    mbar_wait(&full[s], (sd / SS) & 1);
+                    const int nr = min(R, steps - sd * R);
+                    for (int r = 0; r < nr; ++r) {
+                        float* seg = uring + (size_t)(s * R + r) * G::USEG;
+                        const float vl = lo_end > 0 ? seg[i0c] : 0.f;
+                        const float vr = hi_beg < G::UW ? seg[iWc] : 0.f;
+                        __syncwarp();
+                        for (int p = lane; p < lo_end; p += 32) seg[p] = vl;
+                        for (int p = hi_beg + lane; p < G::UW; p += 32) seg[p] = vr;
+                    }
+                    __syncwarp();
+                    mbar_arrive(&ready[s]);
+                }
+            }
             return;
         }
-        const int lo_end = max(0, -useg0);       // segment indices [0, lo_end) are left of column 0
-        const int hi_beg = max(0, a.W - useg0);  // [hi_beg, UW) are right of column W-1
-        const int i0c = lo_end, iWc = a.W - 1 - useg0;
-        for (int st = 0; st < nst + LAG; ++st) {
-            if (st < nst && lane == 0) issue(st);
-            const int sd = st - LAG;
-            if (sd >= 0 && sd < nst) {
-                const int s = sd % SS;
-                mbar_wait(&full[s], (sd / SS) & 1);
-                const int nr = min(R, steps - sd * R);
-                for (int r = 0; r < nr; ++r) {
-                    float* seg = uring + (size_t)(s * R + r) * G::USEG;
-                    const float vl = lo_end > 0 ? seg[i0c] : 0.f;
-                    const float vr = hi_beg < G::UW ? seg[iWc] : 0.f;
-                    __syncwarp();
-                    for (int p = lane; p < lo_end; p += 32) seg[p] = vl;
-                    for (int p = hi_beg + lane; p < G::UW; p += 32) seg[p] = vr;
-                }
-                __syncwarp();
-                mbar_arrive(&ready[s]);
-            }
-        }
-        return;
-    }
 
-    auto qrow_ptr = [&](int r) { return qbuf + (size_t)(r & (QR - 1)) * G::QSEG; };
-    const float scale = a.scale, eps = a.eps;
+        auto qrow_ptr = [&](int r) { return qbuf + (size_t)(r & (QR - 1)) * G::QSEG; };
+        const float scale = a.scale, eps = a.eps;
 
-    if (tid < NT) {  // ---------------------------------- A warps: q rows
-        uint64_t* gate = edge_cta ? ready : full;
-        const int qc = x0 - G::HX + 4 * tid;  // first q column of this thread
-        // q columns outside the image take the clamped column's value: such a
-        // thread computes the 4-column group qcl holding the clamped columns
-        // and picks components (warp-uniform)
-        const int wq0 = x0 - G::HX + 128 * (tid >> 5);
-        const bool edgeA = wq0 < 0 || wq0 + 127 > a.W - 1;
-        const int qcl = min(max(qc, 0), (a.W - 1) & ~3);
-        const int4 sel = make_int4(clampi(qc, 0, a.W - 1) - qcl, clampi(qc + 1, 0, a.W - 1) - qcl,
-                                   clampi(qc + 2, 0, a.W - 1) - qcl, clampi(qc + 3, 0, a.W - 1) - qcl);
-        const int chunk = (qcl - qc) / 4 + tid;
-        const float* fcol = a.f + img + qcl;
-        VRing<MY> r1;
-        int s = 0;
-        unsigned phase = 0;
-        // f for A(i): row j0 + i - RY (clamped: prefetches past the band are unused)
-        auto load_f = [&](int i) { return ldg4(fcol + clampi(j0 + i - RY, qr_lo, qr_hi) * pitch); };
-        // step i: u row j0 + i -> H1 -> vertical window -> q row i - 2 RY.
-        // Steady (ST): ring full, a q row every step, the q slot was used
-        // before, parity ODD known at compile time.
-        // q = f / max(v, eps) with v = col / (MX MY): max.NaN keeps the
-        // reference's NaN propagation; MUFU reciprocal + one Newton step (packed)
-        auto quot4 = [&](const float4 col, const float4 fv) {
-            const float4 v = mul4s(col, scale);
-            const float4 d = make_float4(fmax_nan(v.x, eps), fmax_nan(v.y, eps), fmax_nan(v.z, eps), fmax_nan(v.w, eps));
-            float4 r;
-            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(d.x));
-            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(d.y));
-            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.z) : "f"(d.z));
-            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.w) : "f"(d.w));
-            const float2 q0l = mul2(lo2(fv), lo2(r)), q0h = mul2(hi2(fv), hi2(r));
-#ifdef FDG_FUSED_NO_NEWTON
-            return cat4(q0l, q0h);
-#endif
-            const float2 el = fma2(make_float2(-d.x, -d.y), q0l, lo2(fv));
-            const float2 eh = fma2(make_float2(-d.z, -d.w), q0h, hi2(fv));
-            return cat4(fma2(el, lo2(r), q0l), fma2(eh, hi2(r), q0h));
-        };
-        auto step = [&](auto steady, auto odd, const int i, float4& fx) {
-            constexpr bool ST = decltype(steady)::value;
-            constexpr int ODD = decltype(odd)::value;
-            const bool par = ST ? ODD : (i & 1);
-            if (!par) mbar_wait(&gate[s], phase);
-            float4 h = hsum15x4(uring + (size_t)(s * R + par) * G::USEG, chunk);
-            if (par || (!ST && i == steps - 1)) {  // this thread is done with the stage's u rows
-                mbar_arrive(&empty[s]);
-                if (++s == SS) {
-                    s = 0;
-                    phase ^= 1u;
-                }
-            }
-            if (edgeA) h = pick4(h, sel);
-            if (ST)
-                r1.push_full(v1, NT, tid, h);
-            else
-                r1.push(v1, NT, tid, h);
-            const int r = i - 2 * RY;
-            if (ST || r >= 0) {
-                const float4 fv = edgeA ? pick4(fx, sel) : fx;
-                // f / max(v, eps): max.NaN keeps the reference's NaN propagation
-                const float4 q = quot4(r1.col, fv);
-                if (ST || r >= QR) mbar_wait(&qempty[r & (QR - 1)], ((r / QR) - 1) & 1);
-                *reinterpret_cast<float4*>(qrow_ptr(r) + 4 * tid) = q;
-                mbar_arrive(&qfull[r & (QR - 1)]);
-            }
-            if (!ST) fx = load_f(i + 2);
-        };
-        float4 F0 = load_f(0), F1 = load_f(1);
-        const int i_s = 2 * RY + QR;  // ring full, q rows past the first ring turn
-        // steady blocks end 2 rows before the last q row (prefetch stays in range)
-        const int nblk = steps - 2 > i_s ? (steps - 2 - i_s) / REFRESH : 0;
-        int i = 0;
-        for (; i < (nblk ? i_s : steps); i += 2) {
-            step(std::false_type(), std::integral_constant<int, 0>(), i, F0);
-            if (i + 1 < steps) step(std::false_type(), std::integral_constant<int, 1>(), i + 1, F1);
-        }
-        if (nblk) {
-            const float* fp = fcol + (long long)(j0 + i + 2 - RY) * pitch;  // f row of A(i + 2)
-            for (int b = 0; b < nblk; ++b) {
-#pragma unroll 1
-                for (int t = 0; t < REFRESH; t += 2, i += 2) {
-#ifdef FDG_FUSED_STEPWISE
-                    step(std::true_type(), std::integral_constant<int, 0>(), i, F0);
-                    F0 = ldg4(fp);
-                    step(std::true_type(), std::integral_constant<int, 1>(), i + 1, F1);
-                    F1 = ldg4(fp + pitch);
-#else
-                    // one stage (2 u rows) per iteration: both window sums in
-                    // flight, then both q rows handed to the B warps
-                    mbar_wait(&gate[s], phase);
-                    const float* us = uring + (size_t)(s * R) * G::USEG;
-                    float4 h0 = hsum15x4(us, chunk);
-                    float4 h1 = hsum15x4(us + G::USEG, chunk);
+        if (tid < NT) {  // ---------------------------------- A warps: q rows
+            uint64_t* gate = edge_cta ? ready : full;
+            const int qc = x0 - G::HX + 4 * tid;  // first q column of this thread
+            // q columns outside the image take the clamped column's value: such a
+            // thread computes the 4-column group qcl holding the clamped columns
+            // and picks components (warp-uniform)
+            const int wq0 = x0 - G::HX + 128 * (tid >> 5);
+            const bool edgeA = wq0 < 0 || wq0 + 127 > a.W - 1;
+            const int qcl = min(max(qc, 0), (a.W - 1) & ~3);
+            const int4 sel = make_int4(clampi(qc, 0, a.W - 1) - qcl, clampi(qc + 1, 0, a.W - 1) - qcl,
+                                       clampi(qc + 2, 0, a.W - 1) - qcl, clampi(qc + 3, 0, a.W - 1) - qcl);
+            const int chunk = (qcl - qc) / 4 + tid;
+            const float* fcol = a.f + img + qcl;
+            VRing<MY> r1;
+            int s = 0;
+            unsigned phase = 0;
+            // f for A(i): row j0 + i - RY (clamped: prefetches past the band are unused)
+            auto load_f = [&](int i) { return ldg4(fcol + clampi(j0 + i - RY, qr_lo, qr_hi) * pitch); };
+            // step i: u row j0 + i -> H1 -> vertical window -> q row i - 2 RY.
+            // Steady (ST): ring full, a q row every step, the q slot was used
+            // before, parity ODD known at compile time.
+            // q = f / max(v, eps) with v = col / (MX MY): max.NaN keeps the
+            // reference's NaN propagation; MUFU reciprocal + one Newton step (packed)
+            auto quot4 = [&](const float4 col, const float4 fv) {
+                const float4 v = mul4s(col, scale);
+                const float4 d = make_float4(fmax_nan(v.x, eps), fmax_nan(v.y, eps), fmax_nan(v.z, eps), fmax_nan(v.w, eps));
+                float4 r;
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(d.x));
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(d.y));
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.z) : "f"(d.z));
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.w) : "f"(d.w));
+                const float2 q0l = mul2(lo2(fv), lo2(r)), q0h = mul2(hi2(fv), hi2(r));
+    #ifdef FDG_FUSED_NO_NEWTON
+                return cat4(q0l, q0h);
+    #endif
+                const float2 el = fma2(make_float2(-d.x, -d.y), q0l, lo2(fv));
+                const float2 eh = fma2(make_float2(-d.z, -d.w), q0h, hi2(fv));
+                return cat4(fma2(el, lo2(r), q0l), fma2(eh, hi2(r), q0h));
+            };
+            auto step = [&](auto steady, auto odd, const int i, float4& fx) {
+                constexpr bool ST = decltype(steady)::value;
+                constexpr int ODD = decltype(odd)::value;
+                const bool par = ST ? ODD : (i & 1);
+                if (!par) mbar_wait(&gate[s], phase);
+                float4 h = hsum15x4(uring + (size_t)(s * R + par) * G::USEG, chunk);
+                if (par || (!ST && i == steps - 1)) {  // this thread is done with the stage's u rows
                     mbar_arrive(&empty[s]);
                     if (++s == SS) {
                         s = 0;
                         phase ^= 1u;
                     }
-                    if (edgeA) {
-                        h0 = pick4(h0, sel);
-                        h1 = pick4(h1, sel);
-                    }
-                    r1.push_full(v1, NT, tid, h0);
-                    const float4 qa = quot4(r1.col, edgeA ? pick4(F0, sel) : F0);
-                    r1.push_full(v1, NT, tid, h1);
-                    const float4 qb = quot4(r1.col, edgeA ? pick4(F1, sel) : F1);
-                    F0 = ldg4(fp);
-                    F1 = ldg4(fp + pitch);
-                    const int r = i - 2 * RY;  // even: slots r, r + 1 in the same ring turn
-                    mbar_wait(&qempty[r & (QR - 1)], ((r / QR) - 1) & 1);
-                    mbar_wait(&qempty[(r + 1) & (QR - 1)], (((r + 1) / QR) - 1) & 1);
-                    *reinterpret_cast<float4*>(qrow_ptr(r) + 4 * tid) = qa;
-                    *reinterpret_cast<float4*>(qrow_ptr(r + 1) + 4 * tid) = qb;
+                }
+                if (edgeA) h = pick4(h, sel);
+                if (ST)
+                    r1.push_full(v1, NT, tid, h);
+                else
+                    r1.push(v1, NT, tid, h);
+                const int r = i - 2 * RY;
+                if (ST || r >= 0) {
+                    const float4 fv = edgeA ? pick4(fx, sel) : fx;
+                    // f / max(v, eps): max.NaN keeps the reference's NaN propagation
+                    const float4 q = quot4(r1.col, fv);
+                    if (ST || r >= QR) mbar_wait(&qempty[r & (QR - 1)], ((r / QR) - 1) & 1);
+                    *reinterpret_cast<float4*>(qrow_ptr(r) + 4 * tid) = q;
                     mbar_arrive(&qfull[r & (QR - 1)]);
-                    mbar_arrive(&qfull[(r + 1) & (QR - 1)]);
-#endif
-                    fp += 2 * pitch;
                 }
-                r1.refresh(v1, NT, tid);  // fp32 drift
+                if (!ST) fx = load_f(i + 2);
+            };
+            float4 F0 = load_f(0), F1 = load_f(1);
+            const int i_s = 2 * RY + QR;  // ring full, q rows past the first ring turn
+            // steady blocks end 2 rows before the last q row (prefetch stays in range)
+            const int nblk = steps - 2 > i_s ? (steps - 2 - i_s) / REFRESH : 0;
+            int i = 0;
+            for (; i < (nblk ? i_s : steps); i += 2) {
+                step(std::false_type(), std::integral_constant<int, 0>(), i, F0);
+                if (i + 1 < steps) step(std::false_type(), std::integral_constant<int, 1>(), i + 1, F1);
             }
-            r1.n += nblk * REFRESH;
-        }
-        for (; i < steps; i += 2) {
-            step(std::false_type(), std::integral_constant<int, 0>(), i, F0);
-            if (i + 1 < steps) step(std::false_type(), std::integral_constant<int, 1>(), i + 1, F1);
-        }
-        return;
-    }
-
-    // ------------------------------------------------ B warps: output rows
-    const int tb = tid - NT;
-    const int lane = tid & 31;
-    const int oc = x0 + 4 * tb;
-    const bool has_out = tb < G::NB && oc < a.W;  // lanes past the strip compute, never store
-    const bool full_store = oc + 3 < a.W;
-    const int ocl = min(oc, a.Wp4 - 4);
-    const float* ucol = a.u_in + img + ocl;
-    float* ocol = a.u_out + img + oc;
-    VRing<MY> r2;
-    float4 hlast = make_float4(0.f, 0.f, 0.f, 0.f);
-    float maxd = 0.f;
-    auto load_u = [&](int o) { return ldg4(ucol + min(yb0 + o, yb1 - 1) * pitch); };  // u of output o
-    auto store = [&](auto fs, const int o, const float4 c, const float4 u) {
-        constexpr bool FS = decltype(fs)::value;
-        const bool fst = FS || full_store;
-        const float4 cu = mul4s(c, scale);
-        float4 v4 = cat4(mul2(lo2(cu), lo2(u)), mul2(hi2(cu), hi2(u)));
-        if (a.clamp)
-            v4 = make_float4(fmax_nan(v4.x, 0.f), fmax_nan(v4.y, 0.f), fmax_nan(v4.z, 0.f), fmax_nan(v4.w, 0.f));
-        const float4 dv = sub4(v4, u);
-        float val[4] = {v4.x, v4.y, v4.z, v4.w};
-        const float dd[4] = {dv.x, dv.y, dv.z, dv.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            if (fst || oc + e < a.W) maxd = fmax_nan(maxd, fabsf(dd[e]));
-        float* outp = ocol + (yb0 + o) * pitch;
-        if (fst) {
-            *reinterpret_cast<float4*>(outp) = make_float4(val[0], val[1], val[2], val[3]);
-        } else {
-            outp[0] = val[0];
-            if (oc + 1 < a.W) outp[1] = val[1];
-            if (oc + 2 < a.W) outp[2] = val[2];
-        }
-    };
-    auto take = [&](int r) {  // H2 of q row r (waits for the A warps, frees the slot)
-        mbar_wait_sleep(&qfull[r & (QR - 1)], (r / QR) & 1, FDG_QSLEEP);
-        const float4 h = hsum15x4(qrow_ptr(r), tb);
-        mbar_arrive(&qempty[r & (QR - 1)]);
-        return h;
-    };
-    // pushes: q rows above the image replicate row 0 (extras), rows below
-    // the image replicate the last one (trailing); output o = push - 2 RY
-    const int extras = qr_lo - (yb0 - RY);
-    const int band = yb1 - yb0;
-    auto push_out = [&](const float4 h, float4 u) {
-        r2.push(v2, NT, tb, h);
-        if (r2.n >= MY && has_out) store(std::false_type(), r2.n - MY, r2.col, u);
-    };
-    // warm-up: q rows 0 .. r_s-1 (ring not yet full)
-    const int r_s = (max(1, 2 * RY + 1 - extras) + 1) & ~1;
-    const int r_e = nq;  // steady: one push and one output per q row
-    const int nblk = r_e > r_s ? (r_e - r_s) / REFRESH : 0;
-    int r = 0;
-    for (; r < min(r_s, nq); ++r) {
-        hlast = take(r);
-        if (r == 0)
-            for (int p = 0; p < extras; ++p) r2.push(v2, NT, tb, hlast);
-        const int o = r2.n + 1 - MY;
-        push_out(hlast, o >= 0 ? load_u(o) : make_float4(0.f, 0.f, 0.f, 0.f));
-    }
-    if (nblk) {
-        // here r2 is full and output o = r + extras - 2 RY follows every push
-        const int o0 = r + extras - 2 * RY;
-        float4 U0 = load_u(o0), U1 = load_u(o0 + 1);
-        auto blocks = [&](auto fs) {
-            for (int b = 0; b < nblk; ++b) {
-#pragma unroll 1
-                for (int t = 0; t < REFRESH; t += 2, r += 2) {
-                    const int o = r + extras - 2 * RY;
-                    const float4 g0 = take(r);
-                    const float4 g1 = take(r + 1);
-                    r2.push_full(v2, NT, tb, g0);
-                    if (has_out) store(fs, o, r2.col, U0);
-                    r2.push_full(v2, NT, tb, g1);
-                    if (has_out) store(fs, o + 1, r2.col, U1);
-                    U0 = load_u(o + 2);
-                    U1 = load_u(o + 3);
-                    hlast = g1;
+            if (nblk) {
+                const float* fp = fcol + (long long)(j0 + i + 2 - RY) * pitch;  // f row of A(i + 2)
+                for (int b = 0; b < nblk; ++b) {
+    #pragma unroll 1
+                    for (int t = 0; t < REFRESH; t += 2, i += 2) {
+    #ifdef FDG_FUSED_STEPWISE
+                        step(std::true_type(), std::integral_constant<int, 0>(), i, F0);
+                        F0 = ldg4(fp);
+                        step(std::true_type(), std::integral_constant<int, 1>(), i + 1, F1);
+                        F1 = ldg4(fp + pitch);
+    #else
+                        // one stage (2 u rows) per iteration: both window sums in
+                        // flight, then both q rows handed to the B warps
+                        mbar_wait(&gate[s], phase);
+                        const float* us = uring + (size_t)(s * R) * G::USEG;
+                        float4 h0 = hsum15x4(us, chunk);
+                        float4 h1 = hsum15x4(us + G::USEG, chunk);
+                        mbar_arrive(&empty[s]);
+                        if (++s == SS) {
+                            s = 0;
+                            phase ^= 1u;
+                        }
+                        if (edgeA) {
+                            h0 = pick4(h0, sel);
+                            h1 = pick4(h1, sel);
+                        }
+                        r1.push_full(v1, NT, tid, h0);
+                        const float4 qa = quot4(r1.col, edgeA ? pick4(F0, sel) : F0);
+                        r1.push_full(v1, NT, tid, h1);
+                        const float4 qb = quot4(r1.col, edgeA ? pick4(F1, sel) : F1);
+                        F0 = ldg4(fp);
+                        F1 = ldg4(fp + pitch);
+                        const int r = i - 2 * RY;  // even: slots r, r + 1 in the same ring turn
+                        mbar_wait(&qempty[r & (QR - 1)], ((r / QR) - 1) & 1);
+                        mbar_wait(&qempty[(r + 1) & (QR - 1)], (((r + 1) / QR) - 1) & 1);
+                        *reinterpret_cast<float4*>(qrow_ptr(r) + 4 * tid) = qa;
+                        *reinterpret_cast<float4*>(qrow_ptr(r + 1) + 4 * tid) = qb;
+                        mbar_arrive(&qfull[r & (QR - 1)]);
+                        mbar_arrive(&qfull[(r + 1) & (QR - 1)]);
+    #endif
+                        fp += 2 * pitch;
+                    }
+                    r1.refresh(v1, NT, tid);  // fp32 drift
                 }
-                r2.refresh(v2, NT, tb);  // fp32 drift
+                r1.n += nblk * REFRESH;
+            }
+            for (; i < steps; i += 2) {
+                step(std::false_type(), std::integral_constant<int, 0>(), i, F0);
+                if (i + 1 < steps) step(std::false_type(), std::integral_constant<int, 1>(), i + 1, F1);
+            }
+            return;
+        }
+
+        // ------------------------------------------------ B warps: output rows
+        const int tb = tid - NT;
+        const int lane = tid & 31;
+        const int oc = x0 + 4 * tb;
+        const bool has_out = tb < G::NB && oc < a.W;  // lanes past the strip compute, never store
+        const bool full_store = oc + 3 < a.W;
+        const int ocl = min(oc, a.Wp4 - 4);
+        const float* ucol = a.u_in + img + ocl;
+        float* ocol = a.u_out + img + oc;
+        VRing<MY> r2;
+        float4 hlast = make_float4(0.f, 0.f, 0.f, 0.f);
+        float maxd = 0.f;
+        auto load_u = [&](int o) { return ldg4(ucol + min(yb0 + o, yb1 - 1) * pitch); };  // u of output o
+        auto store = [&](auto fs, const int o, const float4 c, const float4 u) {
+            constexpr bool FS = decltype(fs)::value;
+            const bool fst = FS || full_store;
+            const float4 cu = mul4s(c, scale);
+            float4 v4 = cat4(mul2(lo2(cu), lo2(u)), mul2(hi2(cu), hi2(u)));
+            if (a.clamp)
+                v4 = make_float4(fmax_nan(v4.x, 0.f), fmax_nan(v4.y, 0.f), fmax_nan(v4.z, 0.f), fmax_nan(v4.w, 0.f));
+            const float4 dv = sub4(v4, u);
+            float val[4] = {v4.x, v4.y, v4.z, v4.w};
+            const float dd[4] = {dv.x, dv.y, dv.z, dv.w};
+    #pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (fst || oc + e < a.W) maxd = fmax_nan(maxd, fabsf(dd[e]));
+            float* outp = ocol + (yb0 + o) * pitch;
+            if (fst) {
+                *reinterpret_cast<float4*>(outp) = make_float4(val[0], val[1], val[2], val[3]);
+            } else {
+                outp[0] = val[0];
+                if (oc + 1 < a.W) outp[1] = val[1];
+                if (oc + 2 < a.W) outp[2] = val[2];
             }
         };
-        if (x0 + G::CW <= a.W)
-            blocks(std::true_type());  // every B lane owns 4 image columns
-        else
-            blocks(std::false_type());
-        r2.n += nblk * REFRESH;
-    }
-    for (; r < nq; ++r) {
-        hlast = take(r);
-        push_out(hlast, load_u(r2.n + 1 - MY));
-    }
-    while (r2.n - 2 * RY < band) push_out(hlast, load_u(r2.n + 1 - MY));  // below the image
-
-    if (a.maxchange) {
-        const bool nan = isnan(maxd);
-        const unsigned bits = __reduce_max_sync(0xffffffffu, nan ? 0u : __float_as_uint(maxd));
-        const int anynan = __reduce_or_sync(0xffffffffu, (int)nan);
-        if (lane == 0) {
-            if (bits) atomicMax(a.maxchange, bits);
-            if (anynan) atomicOr(a.nanflag, 1);
+        auto take = [&](int r) {  // H2 of q row r (waits for the A warps, frees the slot)
+            mbar_wait_sleep(&qfull[r & (QR - 1)], (r / QR) & 1, FDG_QSLEEP);
+            const float4 h = hsum15x4(qrow_ptr(r), tb);
+            mbar_arrive(&qempty[r & (QR - 1)]);
+            return h;
+        };
+        // pushes: q rows above the image replicate row 0 (extras), rows below
+        // the image replicate the last one (trailing); output o = push - 2 RY
+        const int extras = qr_lo - (yb0 - RY);
+        const int band = yb1 - yb0;
+        auto push_out = [&](const float4 h, float4 u) {
+            r2.push(v2, NT, tb, h);
+            if (r2.n >= MY && has_out) store(std::false_type(), r2.n - MY, r2.col, u);
+        };
+        // warm-up: q rows 0 .. r_s-1 (ring not yet full)
+        const int r_s = (max(1, 2 * RY + 1 - extras) + 1) & ~1;
+        const int r_e = nq;  // steady: one push and one output per q row
+        const int nblk = r_e > r_s ? (r_e - r_s) / REFRESH : 0;
+        int r = 0;
+        for (; r < min(r_s, nq); ++r) {
+            hlast = take(r);
+            if (r == 0)
+                for (int p = 0; p < extras; ++p) r2.push(v2, NT, tb, hlast);
+            const int o = r2.n + 1 - MY;
+            push_out(hlast, o >= 0 ? load_u(o) : make_float4(0.f, 0.f, 0.f, 0.f));
         }
+        if (nblk) {
+            // here r2 is full and output o = r + extras - 2 RY follows every push
+            const int o0 = r + extras - 2 * RY;
+            float4 U0 = load_u(o0), U1 = load_u(o0 + 1);
+            auto blocks = [&](auto fs) {
+                for (int b = 0; b < nblk; ++b) {
+    #pragma unroll 1
+                    for (int t = 0; t < REFRESH; t += 2, r += 2) {
+                        const int o = r + extras - 2 * RY;
+                        const float4 g0 = take(r);
+                        const float4 g1 = take(r + 1);
+                        r2.push_full(v2, NT, tb, g0);
+                        if (has_out) store(fs, o, r2.col, U0);
+                        r2.push_full(v2, NT, tb, g1);
+                        if (has_out) store(fs, o + 1, r2.col, U1);
+                        U0 = load_u(o + 2);
+                        U1 = load_u(o + 3);
+                        hlast = g1;
+                    }
+                    r2.refresh(v2, NT, tb);  // fp32 drift
+                }
+            };
+            if (x0 + G::CW <= a.W)
+                blocks(std::true_type());  // every B lane owns 4 image columns
+            else
+                blocks(std::false_type());
+            r2.n += nblk * REFRESH;
+        }
+        for (; r < nq; ++r) {
+            hlast = take(r);
+            push_out(hlast, load_u(r2.n + 1 - MY));
+        }
+        while (r2.n - 2 * RY < band) push_out(hlast, load_u(r2.n + 1 - MY));  // below the image
+
+        if (a.maxchange) {
+            const bool nan = isnan(maxd);
+            const unsigned bits = __reduce_max_sync(0xffffffffu, nan ? 0u : __float_as_uint(maxd));
+            const int anynan = __reduce_or_sync(0xffffffffu, (int)nan);
+            if (lane == 0) {
+                if (bits) atomicMax(a.maxchange, bits);
+                if (anynan) atomicOr(a.nanflag, 1);
+            }
+        }
+    };
+    auto reset_barriers = [&]() {  // between segments: every role is done with them
+        __syncthreads();
+        if (tid == 0) {
+            for (int s = 0; s < 3 * SS + 2 * QR; ++s) mbar_inval(full + s);
+        }
+        __syncthreads();
+    };
+    // Work of this CTA as a range [p, end) of the strip-major sequence of
+    // (strip, row) pairs.  Plain grid: strip blockIdx.x, one row band.
+    // Work-balanced (lin_len > 0): rows [b L, (b + 1) L) of the sequence,
+    // possibly the tail of one strip and the head of the next, so every
+    // resident CTA slot gets the same work (the plain grid leaves slots idle
+    // when strips x bands < SMs x occupancy).  One call site of the segment
+    // body keeps it inlined.
+    const int rows = a.y1 - a.y0;
+    long long p, end;
+    if (a.lin_len > 0) {
+        p = (long long)blockIdx.x * a.lin_len;
+        end = min((long long)a.strips * rows, p + a.lin_len);
+    } else {
+        p = (long long)blockIdx.x * rows + (long long)blockIdx.y * a.band;
+        end = min((long long)blockIdx.x * rows + rows, p + a.band);
+    }
+    for (bool first = true; p < end; first = false) {
+        const int sx = (int)(p / rows), r0 = (int)(p - (long long)sx * rows);
+        const int r1 = (int)min((long long)rows, r0 + (end - p));
+        if (!first) reset_barriers();
+        run_segment(sx * G::CW, a.y0 + r0, a.y0 + r1);
+        p += r1 - r0;
     }
 }
 
@@ -530,6 +561,21 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     a.band = (int)((rows + ctas_y - 1) / ctas_y);
     if (const char* e = getenv("FDG_FUSED_BAND")) a.band = std::max(1, atoi(e));
     dim3 grid(strips, (rows + a.band - 1) / a.band, a.batch);
+    // single images: spread (strip, row) work evenly over every resident CTA
+    // slot when the plain grid leaves slots idle (config 4: 34 strips x 8
+    // bands = 272 of 296 slots)
+    static const bool lin_on = !getenv("FDG_FUSED_LIN") || atoi(getenv("FDG_FUSED_LIN")) != 0;
+    a.lin_len = 0;
+    a.strips = strips;
+    const long long slots = (long long)sms * occ;
+    if (lin_on && a.batch == 1 && grid.x * grid.y < slots) {
+        const long long total = (long long)strips * rows;
+        const long long L = (total + slots - 1) / slots;
+        if (L >= 8 * G::MY) {
+            a.lin_len = (int)L;
+            grid = dim3((unsigned)((total + L - 1) / L), 1, 1);
+        }
+    }
     k_fused<RX, RY, NT, R, S, QR><<<grid, 2 * NT + 32, smem, st>>>(a);
     return cudaGetLastError();
 }
