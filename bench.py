@@ -309,14 +309,20 @@ def run_ours(args, cfg, world, rank, local):
         e2e = {"value": W_ * H_ * iters / e2e_s / 1e6, "unit": "Mpx*it/s", "h2d_bytes_per_step": int(f_host.nbytes),
                "d2h_bytes_per_step": int(res.image.nbytes), "api": "paper_1304_7211_b200.rlDeconvolve (C ABI fdg_rl_deconvolve, host buffers)"}
     elif world == 1:
-        # batch: per-image host API calls, all images each step
+        # batch: per-image host API calls (pinned inputs), all images each step
         ctx = Context(local)
-        a = time.perf_counter()
-        nb = 0
-        for i in range(f_host.shape[0]):
-            res = rlDeconvolve(f_host[i], psf, rl_cfg, ctx=ctx)
-            nb += res.image.nbytes
-        e2e_s = time.perf_counter() - a
+        f_pinned = torch.from_numpy(f_host).pin_memory().numpy()
+        rlDeconvolve(f_pinned[0], psf, rl_cfg, ctx=ctx)  # warm: solver + captured graph (same for every image)
+        e_t = []
+        for _ in range(max(1, min(args.steps, 3))):
+            torch.cuda.synchronize(dev)
+            a = time.perf_counter()
+            nb = 0
+            for i in range(f_pinned.shape[0]):
+                res = rlDeconvolve(f_pinned[i], psf, rl_cfg, ctx=ctx)
+                nb += res.image.nbytes
+            e_t.append(time.perf_counter() - a)
+        e2e_s = statistics.median(e_t)
         e2e = {"value": W_ * H_ * iters * f_host.shape[0] / e2e_s / 1e6, "unit": "Mpx*it/s",
                "h2d_bytes_per_step": int(f_host.nbytes), "d2h_bytes_per_step": int(nb),
                "api": "paper_1304_7211_b200.rlDeconvolve per image (host buffers)"}
