@@ -442,8 +442,8 @@ cudaError_t launch_nt(SpanArgs a, const Geom& g, const Epi& e, cudaStream_t st) 
 // 1 and 2 -- where the marching grid cannot fill 148 SMs; the marching kernel
 // wins on large ones (less halo recompute).  AP: the epilogue operand is
 // loaded into registers before the tile, so its latency overlaps the stencil.
-template <int MODE, class SH, int V, int NTY, bool AP>
-__global__ void __launch_bounds__(32 * NTY) k_spant(const SpanArgs a) {
+template <int MODE, class SH, int V, int NTY, bool AP, int MINB>
+__global__ void __launch_bounds__(32 * NTY, MINB) k_spant(const SpanArgs a) {
     using E = Ext<SH, 32>;
     constexpr int NR = SH::NR;
     constexpr int TW = 128, TH = V * NTY, TR = TH + NR - 1, TC = TW + E::HL + E::HR, TCP = TC + 4;
@@ -566,15 +566,15 @@ __global__ void __launch_bounds__(32 * NTY) k_spant(const SpanArgs a) {
     }
 }
 
-template <int MODE, class SH, int V, int NTY, bool AP>
+template <int MODE, class SH, int V, int NTY, bool AP, int MINB>
 cudaError_t launch_tile_t(const SpanArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
-    cudaError_t err = smem_attr<k_spant<MODE, SH, V, NTY, AP>>();
+    cudaError_t err = smem_attr<k_spant<MODE, SH, V, NTY, AP, MINB>>();
     if (err != cudaSuccess) return err;
-    k_spant<MODE, SH, V, NTY, AP><<<grid, 32 * NTY, smem, st>>>(a);
+    k_spant<MODE, SH, V, NTY, AP, MINB><<<grid, 32 * NTY, smem, st>>>(a);
     return cudaGetLastError();
 }
 
-template <class SH, int V, int NTY, bool AP>
+template <class SH, int V, int NTY, bool AP, int MINB = 1>
 cudaError_t launch_tile(const SpanArgs& a, const Geom& g, const Epi& e, cudaStream_t st) {
     using E = Ext<SH, 32>;
     constexpr int TH = V * NTY;
@@ -583,9 +583,9 @@ cudaError_t launch_tile(const SpanArgs& a, const Geom& g, const Epi& e, cudaStre
     if (rows <= 0) return cudaSuccess;
     dim3 grid((g.W + 127) / 128, (rows + TH - 1) / TH, g.batch);
     switch (e.mode) {
-        case EPI_STORE: return launch_tile_t<EPI_STORE, SH, V, NTY, AP>(a, grid, smem, st);
-        case EPI_QUOT: return launch_tile_t<EPI_QUOT, SH, V, NTY, AP>(a, grid, smem, st);
-        case EPI_UPDATE: return launch_tile_t<EPI_UPDATE, SH, V, NTY, AP>(a, grid, smem, st);
+        case EPI_STORE: return launch_tile_t<EPI_STORE, SH, V, NTY, AP, MINB>(a, grid, smem, st);
+        case EPI_QUOT: return launch_tile_t<EPI_QUOT, SH, V, NTY, AP, MINB>(a, grid, smem, st);
+        case EPI_UPDATE: return launch_tile_t<EPI_UPDATE, SH, V, NTY, AP, MINB>(a, grid, smem, st);
     }
     return cudaErrorInvalidValue;
 }
@@ -618,8 +618,15 @@ cudaError_t launch_shape(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
     const int mode = spans_mode();
     const bool tile = mode ? mode == 1 : px <= 4608ll * 1024;
     if (tile) {
-        if (SH::NR > 16) return launch_tile<SH, 8, 8, false>(a, g, e, st);  // disc: 128 x 64 tiles
-        return launch_tile<SH, 4, 8, true>(a, g, e, st);                    // oblique: 128 x 32, aux prefetch
+        // disc: 128 x 56 tiles, 64 registers forced (4 CTAs = 32 warps per SM;
+        // the register count of this kernel otherwise drifts between builds,
+        // and 3 CTAs/SM costs a second wave).  2048^2: 37 x 16 = 592 tiles =
+        // exactly one wave of 148 x 4 (128 x 64 tiles: 512 = 0.86 wave, 102k;
+        // 128 x 56: 108k Mpx*it/s on config 2)
+        if constexpr (SH::NR > 16)
+            return launch_tile<SH, 7, 8, false, 4>(a, g, e, st);
+        else
+            return launch_tile<SH, 4, 8, true, 4>(a, g, e, st);  // oblique: 128 x 32, aux prefetch, <= 64 registers
     }
     // marching: 256-column strips give more CTAs for the same band on narrow images
     const bool narrow = nt_env ? nt_env == 64 : px <= 8ll << 20;
