@@ -130,7 +130,7 @@ struct DenseW {
     float w[64 * 32];  // mh x MWP row-major, zero padded (8 KB of the 32 KB parameter space)
 };
 
-template <int MWP, int MODE, bool MASKED>
+template <int MWP, int MW, int MODE, bool MASKED>
 __global__ void __launch_bounds__(256, 2) k_dense(const DenseArgs a, const __grid_constant__ DenseW wp) {
     extern __shared__ __align__(16) float sm[];
     float* tile = sm;                  // (TD + mh - 1) rows x ts
@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(256, 2) k_dense(const DenseArgs a, const __gri
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int m = 4 * kc + e;  // window offset of output column 0
+                    if (m >= MW) continue;     // zero padding of the grid (MW < MWP): no FMA
                     const float2 ww = make_float2(wk[e], wk[e]);
                     if ((m & 1) == 0) {
                         p01 = __ffma2_rn(ww, vA[m / 2], p01);
@@ -251,28 +252,28 @@ __global__ void __launch_bounds__(256, 2) k_dense(const DenseArgs a, const __gri
     if (MODE == EPI_UPDATE || MODE == EPI_MUPDATE) trace_flush(a.e, tr);
 }
 
-template <int MWP, int MODE, bool MASKED>
+template <int MWP, int MW, int MODE, bool MASKED>
 cudaError_t launch_dense_t(const DenseArgs& a, const DenseW& w, dim3 grid, size_t smem, cudaStream_t st) {
-    cudaError_t err = smem_attr<k_dense<MWP, MODE, MASKED>>();
+    cudaError_t err = smem_attr<k_dense<MWP, MW, MODE, MASKED>>();
     if (err != cudaSuccess) return err;
-    k_dense<MWP, MODE, MASKED><<<grid, 256, smem, st>>>(a, w);
+    k_dense<MWP, MW, MODE, MASKED><<<grid, 256, smem, st>>>(a, w);
     return cudaGetLastError();
 }
 
-template <int MWP>
+template <int MWP, int MW = MWP>
 cudaError_t dense_mode(const DenseArgs& a, const DenseW& w, int mode, bool masked, dim3 grid, size_t smem,
                        cudaStream_t st) {
     if (!masked) {
         switch (mode) {
-            case EPI_STORE: return launch_dense_t<MWP, EPI_STORE, false>(a, w, grid, smem, st);
-            case EPI_QUOT: return launch_dense_t<MWP, EPI_QUOT, false>(a, w, grid, smem, st);
-            case EPI_UPDATE: return launch_dense_t<MWP, EPI_UPDATE, false>(a, w, grid, smem, st);
+            case EPI_STORE: return launch_dense_t<MWP, MW, EPI_STORE, false>(a, w, grid, smem, st);
+            case EPI_QUOT: return launch_dense_t<MWP, MW, EPI_QUOT, false>(a, w, grid, smem, st);
+            case EPI_UPDATE: return launch_dense_t<MWP, MW, EPI_UPDATE, false>(a, w, grid, smem, st);
         }
     } else {
         switch (mode) {
-            case EPI_STORE: return launch_dense_t<MWP, EPI_STORE, true>(a, w, grid, smem, st);
-            case EPI_MQUOT: return launch_dense_t<MWP, EPI_MQUOT, true>(a, w, grid, smem, st);
-            case EPI_MUPDATE: return launch_dense_t<MWP, EPI_MUPDATE, true>(a, w, grid, smem, st);
+            case EPI_STORE: return launch_dense_t<MWP, MW, EPI_STORE, true>(a, w, grid, smem, st);
+            case EPI_MQUOT: return launch_dense_t<MWP, MW, EPI_MQUOT, true>(a, w, grid, smem, st);
+            case EPI_MUPDATE: return launch_dense_t<MWP, MW, EPI_MUPDATE, true>(a, w, grid, smem, st);
         }
     }
     return cudaErrorInvalidValue;
@@ -365,7 +366,9 @@ cudaError_t launch_dense(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
         case 4: return dense_mode<4>(a, w, e.mode, masked, grid, smem, st);
         case 8: return dense_mode<8>(a, w, e.mode, masked, grid, smem, st);
         case 16: return dense_mode<16>(a, w, e.mode, masked, grid, smem, st);
-        case 32: return dense_mode<32>(a, w, e.mode, masked, grid, smem, st);
+        case 32:  // 31-wide grids (config 3) skip the padded column's FMAs
+            return p.mw == 31 ? dense_mode<32, 31>(a, w, e.mode, masked, grid, smem, st)
+                              : dense_mode<32>(a, w, e.mode, masked, grid, smem, st);
     }
     return cudaErrorInvalidValue;
 }
