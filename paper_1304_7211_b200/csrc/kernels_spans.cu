@@ -623,10 +623,14 @@ cudaError_t launch_shape(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
         // and 3 CTAs/SM costs a second wave).  2048^2: 37 x 16 = 592 tiles =
         // exactly one wave of 148 x 4 (128 x 64 tiles: 512 = 0.86 wave, 102k;
         // 128 x 56: 108k Mpx*it/s on config 2)
-        if constexpr (SH::NR > 16)
+        if constexpr (SH::NR > 16) {
             return launch_tile<SH, 7, 8, false, 4>(a, g, e, st);
-        else
-            return launch_tile<SH, 4, 8, true, 4>(a, g, e, st);  // oblique: 128 x 32, aux prefetch, <= 64 registers
+        } else {
+            // oblique: 128 x 28 tiles (7 warps x 4 rows), aux prefetch, <= 64
+            // registers; 1024^2: 37 x 8 = 296 tiles = 2 per SM (128 x 32:
+            // 256 tiles, 1-2 per SM: 83.0k; 128 x 28: 85.2k Mpx*it/s)
+            return launch_tile<SH, 4, 7, true, 4>(a, g, e, st);
+        }
     }
     // marching: 256-column strips give more CTAs for the same band on narrow images
     const bool narrow = nt_env ? nt_env == 64 : px <= 8ll << 20;
