@@ -25,7 +25,7 @@ only collective; batches need none.
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Callable, List, Optional
+from typing import Callable, List, Optional, Tuple
 
 import torch
 import torch.distributed as dist
@@ -70,8 +70,16 @@ def psf_halo(psf) -> int:
 def exchange(buf: torch.Tensor, s: Strip, group=None):
     """Swap T boundary core rows with rank-1 / rank+1 (no wrap-around).
     buf: (rows, pitch) with the core at rows [T, T + core)."""
+    for r in exchange_async(buf, s, group):
+        r.wait()
+
+
+def exchange_async(buf: torch.Tensor, s: Strip, group=None) -> list:
+    """Post the halo exchange of `exchange` and return the pending works
+    (NCCL runs them on its own stream; ``work.wait()`` orders the caller's
+    current stream after them)."""
     if s.world == 1 or s.halo == 0:
-        return
+        return []
     T, c = s.halo, s.core
     ops = []
     if s.rank > 0:
@@ -80,8 +88,7 @@ def exchange(buf: torch.Tensor, s: Strip, group=None):
     if s.rank < s.world - 1:
         ops.append(dist.P2POp(dist.isend, buf[c:c + T], s.rank + 1, group))
         ops.append(dist.P2POp(dist.irecv, buf[T + c:T + c + T], s.rank + 1, group))
-    for r in dist.batch_isend_irecv(ops):
-        r.wait()
+    return dist.batch_isend_irecv(ops)
 
 
 class GpuPasses:
@@ -104,11 +111,13 @@ class GpuFused:
     def __init__(self, solver):
         self.solver = solver
 
-    def __call__(self, f: torch.Tensor, u_in: torch.Tensor, u_out: torch.Tensor, s: Strip, k: int):
+    def __call__(self, f: torch.Tensor, u_in: torch.Tensor, u_out: torch.Tensor, s: Strip, k: int,
+                 rows: Optional[Tuple[int, int]] = None):
         pitch = f.shape[-1]
         off = s.halo * pitch * 4
+        y0, y1 = rows if rows is not None else (0, s.core)
         self.solver.iterate(f.data_ptr() + off, u_in.data_ptr() + off, u_out.data_ptr() + off, pitch,
-                            s.rows * pitch, 0, s.core, s.ylo, s.yhi, k)
+                            s.rows * pitch, y0, y1, s.ylo, s.yhi, k)
 
 
 def fused_halo(psf) -> int:
@@ -118,22 +127,38 @@ def fused_halo(psf) -> int:
 
 
 def rl_strips_fused(f_local: torch.Tensor, s: Strip, iterations: int, fused: Callable, group=None,
-                    u: Optional[torch.Tensor] = None, u2: Optional[torch.Tensor] = None) -> torch.Tensor:
+                    u: Optional[torch.Tensor] = None, u2: Optional[torch.Tensor] = None,
+                    overlap: bool = True) -> torch.Tensor:
     """RL on this rank's strip with one exchange per iteration: the 2T-row
     u halo (s.halo = fused_halo(psf)), then one fused iteration that
     recomputes the q rows next to the core ("exchange 14 rows of
     u once and recompute v and q on the halo rows").  f's halo rows are
     filled once (the q rows beyond the core read them).  u ping-pongs
-    between two buffers; returns the one holding the result."""
+    between two buffers; returns the one holding the result.
+
+    overlap: the exchange is posted first and the interior rows
+    [halo, core - halo) -- whose windows stay inside the core -- are computed
+    while it is in flight; the two boundary bands follow once it has landed
+    (the executor takes an output row range)."""
     if u is None:
         u = torch.empty_like(f_local)
     if u2 is None:
         u2 = torch.empty_like(f_local)
     exchange(f_local, s, group)
     u.copy_(f_local)
+    H = s.halo
+    split = overlap and s.world > 1 and H > 0 and s.core > 2 * H
     for k in range(iterations):
-        exchange(u, s, group)
-        fused(f_local, u, u2, s, k)
+        if split:
+            works = exchange_async(u, s, group)
+            fused(f_local, u, u2, s, k, rows=(H, s.core - H))
+            for w in works:
+                w.wait()
+            fused(f_local, u, u2, s, k, rows=(0, H))
+            fused(f_local, u, u2, s, k, rows=(s.core - H, s.core))
+        else:
+            exchange(u, s, group)
+            fused(f_local, u, u2, s, k)
         u, u2 = u2, u
     return u
 

@@ -107,19 +107,24 @@ def test_fused_strips_match_whole_image():
             a[T + c:2 * T + c] = b[T:2 * T]
 
     exchange(fs)
-    us = [x.clone() for x in fs]
-    u2 = [torch.empty_like(x) for x in fs]
     run = S.GpuFused(solver)
-    for k in range(it):
-        exchange(us)
-        for r, s in enumerate(strips):
-            run(fs[r], us[r], u2[r], s, k)
-        us, u2 = u2, us
-    torch.cuda.synchronize()
-    got = np.concatenate([us[r][T:T + s.core, :w].cpu().numpy() for r, s in enumerate(strips)])
-    assert W.max_rel(got, whole) <= 1e-5
-    ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, it, O.BOX2D_SLIDING)
-    assert W.max_rel(got, ref) <= MAX_REL
+    for split in (False, True):  # split: interior rows, then the two boundary bands (the overlapped driver)
+        us = [x.clone() for x in fs]
+        u2 = [torch.empty_like(x) for x in fs]
+        for k in range(it):
+            exchange(us)
+            for r, s in enumerate(strips):
+                if split:
+                    for rows in ((T, s.core - T), (0, T), (s.core - T, s.core)):
+                        run(fs[r], us[r], u2[r], s, k, rows=rows)
+                else:
+                    run(fs[r], us[r], u2[r], s, k)
+            us, u2 = u2, us
+        torch.cuda.synchronize()
+        got = np.concatenate([us[r][T:T + s.core, :w].cpu().numpy() for r, s in enumerate(strips)])
+        assert W.max_rel(got, whole) <= 1e-5
+        ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, it, O.BOX2D_SLIDING)
+        assert W.max_rel(got, ref) <= MAX_REL
 
 
 def test_fused_iterate_rejects_non_fused_solver():

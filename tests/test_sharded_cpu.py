@@ -43,21 +43,25 @@ class OracleFused:
     def __init__(self, psf, op, eps=1e-8):
         self.psf, self.adj, self.op, self.eps = psf, adjoint(psf), op, eps
 
-    def __call__(self, f, u_in, u_out, s, k):
+    def __call__(self, f, u_in, u_out, s, k, rows=None):
+        """Output rows [y0, y1) of the core; reads only u rows within 2T of
+        them (so the interior pass never touches halo rows in flight)."""
         T2, w = s.halo, self.width
         T = T2 // 2
-        img = u_in[T2 + s.ylo:T2 + s.yhi + 1, :w].numpy()
-        v = O.convolve(img, self.psf, self.op)
-        qlo, qhi = max(s.ylo, -T), min(s.yhi, s.core - 1 + T)
-        vq = v[qlo - s.ylo:qhi - s.ylo + 1]
+        y0, y1 = rows if rows is not None else (0, s.core)
+        rlo, rhi = max(s.ylo, y0 - T2), min(s.yhi, y1 - 1 + T2)   # u rows read
+        img = u_in[T2 + rlo:T2 + rhi + 1, :w].numpy()
+        v = O.convolve(img, self.psf, self.op)   # replicate-clamped at rlo / rhi
+        qlo, qhi = max(s.ylo, y0 - T), min(s.yhi, y1 - 1 + T)     # q rows needed
+        vq = v[qlo - rlo:qhi - rlo + 1]
         fq = f[T2 + qlo:T2 + qhi + 1, :w].numpy()
         qb = fq / np.where(vq < self.eps, self.eps, vq)
-        c = O.convolve(qb, self.adj, self.op)[-qlo:-qlo + s.core]
-        uc = u_in[T2:T2 + s.core, :w].numpy()
-        u_out[T2:T2 + s.core, :w] = torch.from_numpy(np.maximum(c * uc, 0.0))
+        c = O.convolve(qb, self.adj, self.op)[y0 - qlo:y1 - qlo]
+        uc = u_in[T2 + y0:T2 + y1, :w].numpy()
+        u_out[T2 + y0:T2 + y1, :w] = torch.from_numpy(np.maximum(c * uc, 0.0))
 
 
-def _worker(rank, world, port, case, H, W_, it, q, fused=False):
+def _worker(rank, world, port, case, H, W_, it, q, fused=False, overlap=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -69,7 +73,7 @@ def _worker(rank, world, port, case, H, W_, it, q, fused=False):
         fl = S.load_strip(f, s, W_ + 3, dtype=torch.float64)
         ex = OracleFused(psf, op) if fused else OraclePasses(psf, op)
         ex.width = W_
-        u = S.rl_strips_fused(fl, s, it, ex) if fused else S.rl_strips(fl, s, it, ex)
+        u = S.rl_strips_fused(fl, s, it, ex, overlap=overlap) if fused else S.rl_strips(fl, s, it, ex)
         full = S.gather_strips(u, s, W_)
         if rank == 0:
             ref, _, _ = O.rl_deconvolve(f, psf, it, op)
@@ -107,14 +111,16 @@ def test_two_rank_strips_equal_single_image(name):
     assert err < 1e-12, err
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_fused_strips_equal_single_image(world):
+@pytest.mark.parametrize("world,overlap", [(2, True), (3, True), (2, False)])
+def test_fused_strips_equal_single_image(world, overlap):
     """The fused strip driver (2T-row u halo, one exchange per iteration,
-    q recomputed next to the core) gives the single-image result."""
+    q recomputed next to the core) gives the single-image result -- also
+    with the exchange overlapped by the interior rows (boundary bands after
+    it lands)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, "box3x5-box2d", 61, 23, 6, q, True))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, "box3x5-box2d", 61, 23, 6, q, True, overlap))
              for r in range(world)]
     for p in procs:
         p.start()
