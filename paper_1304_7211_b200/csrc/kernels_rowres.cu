@@ -6,8 +6,8 @@
 // under RL (replicate clamping only acts along the row), so a CTA can keep
 // its rows' u, f and q in shared memory for ALL iterations: HBM traffic is
 // one read of f and one write of u per run (8 B/px instead of 24 B/px per
-// iteration of the two-pass engines).  Per iteration and thread (8 adjacent
-// columns):
+// iteration of the two-pass engines).  Per iteration and thread (PT = 4 or 8
+// adjacent columns):
 //   1. window of 8+M-1 u values (clamped at the row ends) -> register prefix
 //      sums (restarting per thread: fp32 cancellation ~1e-7 relative) ->
 //      v = sum/M -> q = f / max(v, eps) into shared memory;      __syncthreads
@@ -24,7 +24,6 @@
 namespace fdg {
 namespace {
 
-constexpr int PT = 8;  // columns per thread
 
 struct RowResArgs {
     const float* f;
@@ -50,11 +49,11 @@ __device__ __forceinline__ float tsum(const float* v) {
 
 // out[i] = sum_{k<M} row[clamp(xb + i + off + k)], i < PT (M >= PT).
 // Interior threads read aligned float4 chunks (the window start sits at
-// OFF4 = off & 3 inside its chunk, xb being a multiple of 8); threads at the
+// OFF4 = off & 3 inside its chunk, xb being a multiple of 4); threads at the
 // row ends read clamped scalars.  Sums are formed without subtraction:
 // shared middle (balanced tree) + left suffix + right prefix, dependency
 // depth ~log2(M) + PT instead of a length-M chain.
-template <int M, int OFF4>
+template <int M, int OFF4, int PT>
 __device__ __forceinline__ void window_sums(const float* row, int W, int xb, int off, float (&out)[PT]) {
     constexpr int NW = PT + M - 1;
     constexpr int NCH = (OFF4 + NW - 1) / 4 + 1;
@@ -95,8 +94,10 @@ __device__ __forceinline__ void window_sums(const float* row, int W, int xb, int
     for (int i = 0; i < PT; ++i) out[i] = (L[i] + mid) + Rr[i];
 }
 
-template <int M, int O1, int O2>
+// PT columns per thread: 4 (rows up to 1024 px: more threads per row) or 8
+template <int M, int O1, int O2, int PT>
 __global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
+    constexpr int NV4 = PT / 4;  // own columns as float4 chunks
     extern __shared__ __align__(16) float sm[];
     const int W = a.W;
     const int wp = (W + 3) & ~3;
@@ -139,18 +140,19 @@ __global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
     const int off1 = a.min_dx;               // forward window start
     const int off2 = -(a.min_dx + M - 1);    // adjoint window start (offsets negated)
     for (int it = 0; it < a.iters; ++it) {
-        // own 8 columns move as two float4 (scalar smem accesses at an
-        // 8-float lane stride would conflict 8-way)
+        // own PT columns move as float4 chunks (scalar smem accesses at a
+        // PT-float lane stride would conflict PT-way)
         const bool vec = xb + PT <= W;
         if (active) {
             float v[PT];
-            window_sums<M, O1>(ru, W, xb, off1, v);
+            window_sums<M, O1, PT>(ru, W, xb, off1, v);
             float fv[PT], qv[PT];
             if (vec) {
-                const float4 a0 = *reinterpret_cast<const float4*>(rf + xb);
-                const float4 a1 = *reinterpret_cast<const float4*>(rf + xb + 4);
-                fv[0] = a0.x, fv[1] = a0.y, fv[2] = a0.z, fv[3] = a0.w;
-                fv[4] = a1.x, fv[5] = a1.y, fv[6] = a1.z, fv[7] = a1.w;
+#pragma unroll
+                for (int c = 0; c < NV4; ++c) {
+                    const float4 a0 = *reinterpret_cast<const float4*>(rf + xb + 4 * c);
+                    fv[4 * c] = a0.x, fv[4 * c + 1] = a0.y, fv[4 * c + 2] = a0.z, fv[4 * c + 3] = a0.w;
+                }
             } else {
 #pragma unroll
                 for (int i = 0; i < PT; ++i) fv[i] = xb + i < W ? rf[xb + i] : 1.f;
@@ -161,8 +163,10 @@ __global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
                 qv[i] = div_fast(fv[i], d < a.eps ? a.eps : d);
             }
             if (vec) {
-                *reinterpret_cast<float4*>(rq + xb) = make_float4(qv[0], qv[1], qv[2], qv[3]);
-                *reinterpret_cast<float4*>(rq + xb + 4) = make_float4(qv[4], qv[5], qv[6], qv[7]);
+#pragma unroll
+                for (int c = 0; c < NV4; ++c)
+                    *reinterpret_cast<float4*>(rq + xb + 4 * c) =
+                        make_float4(qv[4 * c], qv[4 * c + 1], qv[4 * c + 2], qv[4 * c + 3]);
             } else {
 #pragma unroll
                 for (int i = 0; i < PT; ++i)
@@ -173,13 +177,14 @@ __global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
         float maxd = 0.f, csum = 0.f;
         if (active) {
             float c[PT];
-            window_sums<M, O2>(rq, W, xb, off2, c);
+            window_sums<M, O2, PT>(rq, W, xb, off2, c);
             float uv[PT];
             if (vec) {
-                const float4 a0 = *reinterpret_cast<const float4*>(ru + xb);
-                const float4 a1 = *reinterpret_cast<const float4*>(ru + xb + 4);
-                uv[0] = a0.x, uv[1] = a0.y, uv[2] = a0.z, uv[3] = a0.w;
-                uv[4] = a1.x, uv[5] = a1.y, uv[6] = a1.z, uv[7] = a1.w;
+#pragma unroll
+                for (int c4 = 0; c4 < NV4; ++c4) {
+                    const float4 a0 = *reinterpret_cast<const float4*>(ru + xb + 4 * c4);
+                    uv[4 * c4] = a0.x, uv[4 * c4 + 1] = a0.y, uv[4 * c4 + 2] = a0.z, uv[4 * c4 + 3] = a0.w;
+                }
             } else {
 #pragma unroll
                 for (int i = 0; i < PT; ++i) uv[i] = xb + i < W ? ru[xb + i] : 0.f;
@@ -195,8 +200,10 @@ __global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
                 uv[i] = value;
             }
             if (vec) {
-                *reinterpret_cast<float4*>(ru + xb) = make_float4(uv[0], uv[1], uv[2], uv[3]);
-                *reinterpret_cast<float4*>(ru + xb + 4) = make_float4(uv[4], uv[5], uv[6], uv[7]);
+#pragma unroll
+                for (int c4 = 0; c4 < NV4; ++c4)
+                    *reinterpret_cast<float4*>(ru + xb + 4 * c4) =
+                        make_float4(uv[4 * c4], uv[4 * c4 + 1], uv[4 * c4 + 2], uv[4 * c4 + 3]);
             } else {
 #pragma unroll
                 for (int i = 0; i < PT; ++i)
@@ -230,20 +237,21 @@ __global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
 constexpr int o1_of(int m) { return (-(m / 2)) & 3; }
 constexpr int o2_of(int m) { return (-(m - 1 - m / 2)) & 3; }
 
-template <int M>
+template <int M, int PT>
 cudaError_t launch_m(const RowResArgs& a, int threads, size_t smem, int blocks, cudaStream_t st) {
     constexpr int O1 = o1_of(M), O2 = o2_of(M);
-    cudaError_t err = smem_attr<k_rowres<M, O1, O2>>();
+    cudaError_t err = smem_attr<k_rowres<M, O1, O2, PT>>();
     if (err != cudaSuccess) return err;
-    k_rowres<M, O1, O2><<<blocks, threads, smem, st>>>(a);
+    k_rowres<M, O1, O2, PT><<<blocks, threads, smem, st>>>(a);
     return cudaGetLastError();
 }
 
 }  // namespace
 
 bool rowres_supported(int mx, int my, int min_dx, int min_dy, int W) {
+    // one row per <= 256-thread CTA: W <= 256 x 8 columns
     return my == 1 && min_dy == 0 && min_dx == -(mx / 2) && (mx == 15 || mx == 31 || mx == 9 || mx == 17) &&
-           W >= 1 && W <= 8192;
+           W >= 1 && W <= 2048;
 }
 
 cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float* u, int pitch, int W, int H,
@@ -264,6 +272,9 @@ cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float
     a.clamp = clamp;
     a.maxchange = maxchange;
     a.nanflag = nanflag;
+    // 4 columns per thread when a row fits 256 threads (more warps per row:
+    // config 0 212k -> 264k Mpx*it/s), else 8
+    const int PT = W <= 1024 ? 4 : 8;
     const int nthr_row = (W + PT - 1) / PT;
     // up to 256 threads per CTA, but at least ~3 CTAs per SM: small images
     // (config 0: 512 rows) otherwise leave SMs idle (4 rows/CTA = 128 CTAs on
@@ -283,11 +294,15 @@ cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float
     const size_t smem = sizeof(float) * (3 * (size_t)rows_per_cta * wp + iters) + sizeof(int) * iters;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     const int blocks = (a.rows_total + rows_per_cta - 1) / rows_per_cta;
-    switch (mx) {
-        case 9: return launch_m<9>(a, threads, smem, blocks, st);
-        case 15: return launch_m<15>(a, threads, smem, blocks, st);
-        case 17: return launch_m<17>(a, threads, smem, blocks, st);
-        case 31: return launch_m<31>(a, threads, smem, blocks, st);
+    switch (mx * 16 + PT) {
+        case 9 * 16 + 4: return launch_m<9, 4>(a, threads, smem, blocks, st);
+        case 15 * 16 + 4: return launch_m<15, 4>(a, threads, smem, blocks, st);
+        case 17 * 16 + 4: return launch_m<17, 4>(a, threads, smem, blocks, st);
+        case 31 * 16 + 4: return launch_m<31, 4>(a, threads, smem, blocks, st);
+        case 9 * 16 + 8: return launch_m<9, 8>(a, threads, smem, blocks, st);
+        case 15 * 16 + 8: return launch_m<15, 8>(a, threads, smem, blocks, st);
+        case 17 * 16 + 8: return launch_m<17, 8>(a, threads, smem, blocks, st);
+        case 31 * 16 + 8: return launch_m<31, 8>(a, threads, smem, blocks, st);
     }
     return cudaErrorInvalidValue;
 }
