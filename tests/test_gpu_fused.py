@@ -193,3 +193,28 @@ def test_two_pass_strips_match_whole_image(psf_name, op, spans_mode):
         lib().fdg_set_option(b"spans", prev_s)
     got = np.concatenate([us[r][T:T + s.core, :w].cpu().numpy() for r, s in enumerate(strips)])
     assert W.max_rel(got, whole) <= 1e-5  # same engine per strip; fp32 order differs only for box running sums
+
+
+def test_fused_work_balanced_segments():
+    """Images large enough for the work-balanced launch (CTAs take equal
+    ranges of the strip-major (strip, row) sequence, crossing strips): odd
+    sizes, against the oracle."""
+    w, h, it = 4001, 3999, 3
+    f, psf = _input(w, h, 91)
+    res = rlDeconvolve(f, psf, RlConfig(iterations=it, op=K.Box2dSliding))
+    ref, mc, _ = O.rl_deconvolve(f.astype(np.float64), psf, it, O.BOX2D_SLIDING)
+    assert W.max_rel(res.image, ref) <= 2e-5
+    np.testing.assert_allclose([r.maxAbsChange for r in res.trace.records], mc, rtol=2e-2, atol=1e-6)
+
+
+@pytest.mark.parametrize("w", [5, 13, 1023, 1024, 1025, 2048])
+def test_rowres_column_split_edges(w):
+    """Row-resident RL around its 4 / 8 columns-per-thread switch (1024 px)
+    and for widths that are not a multiple of 4, batch of rows."""
+    from paper_1304_7211_b200.psf import makeLinePsf
+    rng = np.random.default_rng(w)
+    f = (rng.random((7, w)) * 0.9 + 0.1).astype(np.float32)
+    psf = makeLinePsf(15)
+    res = rlDeconvolve(f, psf, RlConfig(iterations=12, op=K.Box1dSliding))
+    ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, 12, O.BOX1D_SLIDING)
+    assert W.max_rel(res.image, ref) <= 1e-5
