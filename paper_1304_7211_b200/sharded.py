@@ -97,11 +97,13 @@ class GpuPasses:
     def __init__(self, solver):
         self.solver = solver
 
-    def __call__(self, which: int, src: torch.Tensor, aux: torch.Tensor, out: torch.Tensor, s: Strip, k: int):
+    def __call__(self, which: int, src: torch.Tensor, aux: torch.Tensor, out: torch.Tensor, s: Strip, k: int,
+                 rows: Optional[Tuple[int, int]] = None):
         pitch = src.shape[-1]
         off = s.halo * pitch * 4
+        y0, y1 = rows if rows is not None else (0, s.core)
         self.solver.pass_(which, src.data_ptr() + off, aux.data_ptr() + off, out.data_ptr() + off, pitch,
-                          s.rows * pitch, 0, s.core, s.ylo, s.yhi, k)
+                          s.rows * pitch, y0, y1, s.ylo, s.yhi, k)
 
 
 class GpuFused:
@@ -164,19 +166,38 @@ def rl_strips_fused(f_local: torch.Tensor, s: Strip, iterations: int, fused: Cal
 
 
 def rl_strips(f_local: torch.Tensor, s: Strip, iterations: int, passes: Callable, group=None,
-              u: Optional[torch.Tensor] = None, q: Optional[torch.Tensor] = None) -> torch.Tensor:
+              u: Optional[torch.Tensor] = None, q: Optional[torch.Tensor] = None,
+              overlap: bool = True) -> torch.Tensor:
     """RL on this rank's strip.  f_local: (rows, pitch) with halos (f's halo
-    rows are never read).  Returns u (same layout)."""
+    rows are never read).  Returns u (same layout).
+
+    overlap: each pass posts its halo exchange (u before pass 1, q before
+    pass 2), runs the interior rows [T, core - T) -- whose windows stay
+    inside the core -- while it is in flight, then the two T-row boundary
+    bands (the executor takes an output row range)."""
     if u is None:
         u = torch.empty_like(f_local)
     if q is None:
         q = torch.empty_like(f_local)
     u.copy_(f_local)
+    T = s.halo
+    split = overlap and s.world > 1 and T > 0 and s.core > 2 * T
+
+    def run(which, src, aux, out, k):
+        if not split:
+            exchange(src, s, group)
+            passes(which, src, aux, out, s, k)
+            return
+        works = exchange_async(src, s, group)
+        passes(which, src, aux, out, s, k, rows=(T, s.core - T))
+        for w in works:
+            w.wait()
+        passes(which, src, aux, out, s, k, rows=(0, T))
+        passes(which, src, aux, out, s, k, rows=(s.core - T, s.core))
+
     for k in range(iterations):
-        exchange(u, s, group)
-        passes(1, u, f_local, q, s, k)
-        exchange(q, s, group)
-        passes(2, q, u, u, s, k)
+        run(1, u, f_local, q, k)
+        run(2, q, u, u, k)
     return u
 
 

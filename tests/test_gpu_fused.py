@@ -170,7 +170,6 @@ def test_two_pass_strips_match_whole_image(psf_name, op, spans_mode):
         T = S.psf_halo(psf)
         strips = [S.strip_of(h, nst, r, T) for r in range(nst)]
         fs = [S.load_strip(f, s, pitch, device=dev) for s in strips]
-        us = [x.clone() for x in fs]
         qs = [torch.zeros_like(x) for x in fs]
 
         def exchange(bufs):
@@ -180,19 +179,25 @@ def test_two_pass_strips_match_whole_image(psf_name, op, spans_mode):
                 a[T + c:2 * T + c] = b[T:2 * T]
 
         run = S.GpuPasses(solver)
-        for k in range(it):
-            exchange(us)
-            for r, s in enumerate(strips):
-                run(1, us[r], fs[r], qs[r], s, k)
-            exchange(qs)
-            for r, s in enumerate(strips):
-                run(2, qs[r], us[r], us[r], s, k)
-        torch.cuda.synchronize()
+        results = []
+        for split in (False, True):  # split: interior rows, then the boundary bands (the overlapped driver)
+            us = [x.clone() for x in fs]
+            for k in range(it):
+                for which, src, aux, dst in ((1, us, fs, qs), (2, qs, us, us)):
+                    exchange(src)
+                    for r, s in enumerate(strips):
+                        if split and T > 0 and s.core > 2 * T:
+                            for rows in ((T, s.core - T), (0, T), (s.core - T, s.core)):
+                                run(which, src[r], aux[r], dst[r], s, k, rows=rows)
+                        else:
+                            run(which, src[r], aux[r], dst[r], s, k)
+            torch.cuda.synchronize()
+            results.append(np.concatenate([us[r][T:T + s.core, :w].cpu().numpy() for r, s in enumerate(strips)]))
     finally:
         lib().fdg_set_option(b"fused", prev_f)
         lib().fdg_set_option(b"spans", prev_s)
-    got = np.concatenate([us[r][T:T + s.core, :w].cpu().numpy() for r, s in enumerate(strips)])
-    assert W.max_rel(got, whole) <= 1e-5  # same engine per strip; fp32 order differs only for box running sums
+    for got in results:
+        assert W.max_rel(got, whole) <= 1e-5  # same engine per strip; fp32 order differs only for box running sums
 
 
 def test_fused_work_balanced_segments():

@@ -22,17 +22,20 @@ class OraclePasses:
     def __init__(self, psf, op, eps=1e-8):
         self.psf, self.adj, self.op, self.eps = psf, adjoint(psf), op, eps
 
-    def __call__(self, which, src, aux, out, s, k):
+    def __call__(self, which, src, aux, out, s, k, rows=None):
+        """Output rows [y0, y1) of the core; reads only src rows within T of them."""
         T, w = s.halo, self.width
-        img = src[T + s.ylo:T + s.yhi + 1, :w].numpy()
+        y0, y1 = rows if rows is not None else (0, s.core)
+        rlo, rhi = max(s.ylo, y0 - T), min(s.yhi, y1 - 1 + T)
+        img = src[T + rlo:T + rhi + 1, :w].numpy()
         conv = O.convolve(img, self.psf if which == 1 else self.adj, self.op)
-        v = conv[-s.ylo:-s.ylo + s.core]
-        a = aux[T:T + s.core, :w].numpy()
+        v = conv[y0 - rlo:y1 - rlo]
+        a = aux[T + y0:T + y1, :w].numpy()
         if which == 1:
             res = a / np.where(v < self.eps, self.eps, v)
         else:
             res = np.maximum(v * a, 0.0)
-        out[T:T + s.core, :w] = torch.from_numpy(res)
+        out[T + y0:T + y1, :w] = torch.from_numpy(res)
 
 
 class OracleFused:
@@ -73,7 +76,7 @@ def _worker(rank, world, port, case, H, W_, it, q, fused=False, overlap=True):
         fl = S.load_strip(f, s, W_ + 3, dtype=torch.float64)
         ex = OracleFused(psf, op) if fused else OraclePasses(psf, op)
         ex.width = W_
-        u = S.rl_strips_fused(fl, s, it, ex, overlap=overlap) if fused else S.rl_strips(fl, s, it, ex)
+        u = S.rl_strips_fused(fl, s, it, ex, overlap=overlap) if fused else S.rl_strips(fl, s, it, ex, overlap=overlap)
         full = S.gather_strips(u, s, W_)
         if rank == 0:
             ref, _, _ = O.rl_deconvolve(f, psf, it, op)
@@ -96,12 +99,14 @@ CASES = {
 }
 
 
-@pytest.mark.parametrize("name", sorted(CASES))
-def test_two_rank_strips_equal_single_image(name):
+@pytest.mark.parametrize("name,overlap", [(n, True) for n in sorted(CASES)] + [("disc5-generic", False)])
+def test_two_rank_strips_equal_single_image(name, overlap):
+    """Two-pass strip driver (u and q halo exchanges), with and without the
+    exchanges overlapped by the interior rows."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, 37, 23, 6, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, 37, 23, 6, q, False, overlap)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
