@@ -8,26 +8,31 @@
 // 12 B/px instead of 24 B/px for the two-pass engines.  u ping-pongs between
 // two planes (neighbouring bands read u_in halos while others write u_out).
 //
-// A CTA owns CW = 4 NT - 16 output columns of a row band and marches down u
-// rows j = qr_lo - RY ... yb1 - 1 + 2 RY (qr_lo..qr_hi = the q rows the band
-// needs, clamped to the image).  A producer warp streams the replicate-clamped
-// u rows (CW + 32 columns) into a shared ring with TMA bulk copies (R rows per
-// mbarrier stage) and prefetches the matching f rows into L2.  NT consumer
-// threads, 4 columns each, run two independent stages per row step i:
-//   A(i)    H1 = horizontal box sum of u row j over the CW + 16 q columns;
-//           vertical running sum over the last MY H1 rows (shared ring) ->
-//           v row j - RY -> q = f / max(v / (MX MY), eps) (columns clamped to
-//           the image) into a double-buffered shared q row;
-//   B(i-1)  H2 = horizontal box sum of the previous q row over the output
-//           columns; pushed into a vertical ring (RY + 1 times for the first
-//           image row, repeated below the last -- replicate clamping of q) ->
-//           c row -> u_out = max(c / (MX MY) * u, 0), max|du| and NaN.
-// A(i) and B(i-1) are independent, so one named barrier per step separates
-// the q-row producer from its consumer and the two chains overlap.  f and the
-// update's u operand are loaded into registers ahead of use (both L2 hits:
-// f prefetched by the producer, u streamed 14 rows earlier).  Window sums are
-// formed by additions only; vertical running sums are rebuilt from their
-// rings every 32 rows (fp32 drift, SURVEY 7 part 1).
+// A CTA owns CW = 4 NT - 16 output columns of a range of rows and marches
+// down u rows j = qr_lo - RY ... yb1 - 1 + 2 RY (qr_lo..qr_hi = the q rows the
+// range needs, clamped to the image).  Warp-specialised CTA, 2 NT + 32 threads:
+//   producer warp  streams the replicate-clamped u rows (CW + 32 columns) into
+//                  a shared ring with TMA bulk copies (R rows per mbarrier
+//                  stage; in edge CTAs it also replicates columns 0 / W-1 into
+//                  the halo) and prefetches the matching f rows into L2;
+//   A warps (NT)   per u row: H1 = horizontal box sum over the CW + 16 q
+//                  columns -> vertical running sum over the last MY H1 rows
+//                  (shared ring) -> v -> q = f / max(v / (MX MY), eps) into a
+//                  QR-row shared q ring (per-slot qfull / qempty mbarriers, A
+//                  runs up to QR rows ahead of B);
+//   B warps (NT)   per q row: H2 = horizontal box sum over the output columns
+//                  -> vertical ring (q rows above / below the image replicated
+//                  by repeated pushes) -> c -> u_out = max(c / (MX MY) * u, 0),
+//                  max|du| and NaN.
+// Packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2).  Window sums are formed by
+// additions only; vertical running sums are rebuilt from their rings every 32
+// rows (fp32 drift, SURVEY 7 part 1).
+//
+// Work distribution: one wave of resident CTAs (2 per SM).  For single images
+// each CTA takes an equal range of the strip-major sequence of (strip, row)
+// pairs -- possibly the tail of one strip and the head of the next, run as two
+// segments with the barriers re-initialised in between -- so no CTA slot idles
+// (config 4: 34 strips x 8 bands would fill only 272 of 296 slots).
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>

@@ -4,32 +4,37 @@
 // oblique line (config 1, 11 rows, 29 taps).  Other row-convex PSFs use the
 // generic "taps" engine.
 //
-// Same streaming structure as the box engine (kernels_rect.cu): a CTA
-// marches down a column strip; a producer warp streams R replicate-clamped
-// input rows (+ halo) and R epilogue-operand rows per mbarrier stage with TMA
-// bulk copies.  In CTAs whose segment reaches past column 0 or W-1 the
-// producer also writes the halo columns the copy does not cover (replicate-
-// clamped, from global memory) before it arrives on the stage barrier, so
-// every consumer runs the same float4 window code.
+// Two kernels (choice by image size in launch_shape):
 //
-// Consumer thread = 4 adjacent columns:
+// * k_spant, the TILE kernel (images <= 4.5 Mpx per launch: configs 1, 2) --
+//   see its comment further down: a CTA loads its output tile + halo into
+//   shared memory and every thread computes 4 columns x V rows.
+//
+// * k_spans, the MARCHING kernel (larger images): same streaming structure
+//   as the box engine (kernels_rect.cu) -- a CTA marches down a column
+//   strip; a producer warp streams R replicate-clamped input rows (+ halo)
+//   and R epilogue-operand rows per mbarrier stage with TMA bulk copies.  In
+//   CTAs whose segment reaches past column 0 or W-1 the producer also writes
+//   the halo columns the copy does not cover (replicate-clamped, from global
+//   memory) before it arrives on the stage barrier, so every consumer runs
+//   the same float4 window code.
+//
+// Both compute a thread's 4 adjacent output columns the same way:
 //   * per input row: float4 window loads, a register prefix sum over the
 //     window (restarted every row, so fp32 cancellation stays ~1e-7
 //     relative -- SURVEY 7 hard part 1), every span's 4 window sums as prefix
 //     differences (static indices);
-//   * scatter: the row's span sums are added into the pending output rows
-//     they feed (output o = i - r for PSF row r), held in a register ring --
-//     the step loop is unrolled by the ring length so every slot is a static
-//     register; each output accumulates one partial per PSF row, in dy order.
+//   * the row's span sums are added into the pending outputs they feed
+//     (output o = i - r for PSF row r), each output accumulating one partial
+//     per PSF row, in dy order -- the two kernels produce bit-identical
+//     results.  The marching kernel keeps the pending outputs in a register
+//     ring (step loop unrolled by the ring length: static slots).
 //
-// The PSF rows are split between G consumer groups (G = 2: rows [0, NR/2]
-// and the rest).  A group only streams the input rows its rows touch, keeps a
-// ring half as long, and runs half as much unrolled code; group 0 hands its
-// partial sum of output o to group 1 through a shared slot (mbarrier pair),
-// group 1 adds it, scales by 1/count and applies the fused quotient / update
-// epilogue (float4 store).  This doubles the warps marching a strip without
-// re-reading halo rows -- the small (L2-resident) configs 1 and 2 are
-// latency-bound, not bandwidth-bound (profiles/r01_spans_notes.md).
+// Marching-kernel option G = 2 (FDG_SPANS_G=2; measured slower on configs 1
+// and 2, profiles/r01_spans_notes.md): the PSF rows are split between two
+// consumer groups that stream only the input rows their rows touch; group 0
+// hands its partial sum of output o to group 1 through a shared slot
+// (mbarrier pair), group 1 adds it and applies the fused epilogue.
 #include <cstdlib>
 
 #include "common.cuh"
