@@ -482,22 +482,27 @@ __global__ void __launch_bounds__(32 * NTY, MINB) k_spant(const SpanArgs a) {
     }
     constexpr int NQ = TC / 4;
     const bool col_interior = sb >= 0 && sb + TC <= a.W;
+    // tile load: interior chunks as asynchronous 16-byte copies (cp.async:
+    // every copy of the thread in flight at once, no register round trip),
+    // chunks that straddle the image edge as clamped scalar loads
     for (int k = threadIdx.x; k < TR * NQ; k += 32 * NTY) {
         const int t = k / NQ, q = k - t * NQ;
         const int row = clampi(yt0 + SH::MINDY + t, a.ylo, a.yhi);
         const float* rp = src + (long long)row * a.pitch;
         const int c = sb + 4 * q;
-        float4 v;
+        float* dst = tile + t * TCP + 4 * q;
         if (col_interior || (c >= 0 && c + 3 < a.W)) {
-            v = __ldg(reinterpret_cast<const float4*>(rp + c));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(rp + c) : "memory");
         } else {
+            float4 v;
             v.x = __ldg(rp + clampi(c, 0, a.W - 1));
             v.y = __ldg(rp + clampi(c + 1, 0, a.W - 1));
             v.z = __ldg(rp + clampi(c + 2, 0, a.W - 1));
             v.w = __ldg(rp + clampi(c + 3, 0, a.W - 1));
+            *reinterpret_cast<float4*>(dst) = v;
         }
-        *reinterpret_cast<float4*>(tile + t * TCP + 4 * q) = v;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     float4 acc[V];
 #pragma unroll

@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(256, 2) k_dense(const DenseArgs a, const __gri
     const int c0 = cbase & ~3;  // <= cbase (also for negative cbase)
     const int sh = cbase - c0;  // tile column of chunk element k: 4 q + k - sh
     const int nq = (tw + sh + 3) / 4;
-    for (int i = tid; i < th * nq; i += 256) {
+#pragma unroll 4
+    for (int i = tid; i < th * nq; i += 256) {  // unrolled: 4 loads in flight per thread
         const int ty = i / nq, q = i - ty * nq;
         const int gy = clampi(oy0 + a.min_dy + ty, a.ylo, a.yhi);
         const float* rp = in + (long long)gy * a.pitch;
