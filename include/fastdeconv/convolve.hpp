@@ -61,9 +61,11 @@ inline void check(int status) {
     if (status != FDG_OK) raise(status);
 }
 
-/// Process-wide device context (device 0, private stream), created on first use.
+/// Per-thread device context (device 0, private stream and scratch), created
+/// on first use: concurrent calls from different threads share nothing
+/// (the reference API is pure and reentrant).
 inline fdg_ctx* context() {
-    static std::shared_ptr<fdg_ctx> ctx = [] {
+    thread_local std::shared_ptr<fdg_ctx> ctx = [] {
         fdg_ctx* c = nullptr;
         check(fdg_ctx_create(0, &c));
         return std::shared_ptr<fdg_ctx>(c, fdg_ctx_destroy);

@@ -190,9 +190,11 @@ class Desc:
 
 
 class Context:
-    """fdg_ctx: a device + stream.  One default context per device."""
+    """fdg_ctx: a device + stream + scratch.  One default context per device
+    and thread: calls from different threads never share buffers or streams
+    (the reference API is reentrant)."""
 
-    _default = {}
+    _tls = threading.local()
 
     def __init__(self, device: int = 0):
         L = lib()
@@ -214,9 +216,12 @@ class Context:
 
     @classmethod
     def default(cls, device: int = 0) -> "Context":
-        ctx = cls._default.get(device)
+        per_thread = getattr(cls._tls, "ctx", None)
+        if per_thread is None:
+            per_thread = cls._tls.ctx = {}
+        ctx = per_thread.get(device)
         if ctx is None:
-            ctx = cls._default[device] = cls(device)
+            ctx = per_thread[device] = cls(device)
         return ctx
 
     def set_stream(self, stream_ptr: int):

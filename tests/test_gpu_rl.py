@@ -238,3 +238,36 @@ def test_validation_first_bad_pixel_order(w, h):
     f.flat[w * h - 1] = -0.5  # the very last pixel (tail chunk)
     with pytest.raises(ValueError, match="nonnegative"):
         rlDeconvolve(f, makeBoxPsf(1, 1), RlConfig(iterations=1))
+
+
+def test_concurrent_calls_from_threads():
+    """The reference API is reentrant (independent calls may run concurrently,
+    SPEC.md:314): each thread gets its own default context (stream, scratch,
+    cached solver), so concurrent calls give the sequential results."""
+    import threading
+    from paper_1304_7211_b200.psf import makeLinePsf
+    rng = np.random.default_rng(21)
+    jobs = [(rng.random((96 + 8 * i, 120 + 4 * i)).astype(np.float32) + 0.05, psf, op)
+            for i, (psf, op) in enumerate([(W.disc_r10(), K.GenericBox), (makeLinePsf(15), K.Box1dSliding),
+                                           (makeBoxPsf(15, 15), K.Box2dSliding), (W.oblique_line(), K.GenericBox),
+                                           (W.gaussian31(seed=3, size=9), K.Naive), (makeDiscPsf(3), K.GenericBox)])]
+    seq = [rlDeconvolve(f, psf, RlConfig(iterations=15, op=op)).image for f, psf, op in jobs]
+    out = [None] * len(jobs)
+    errs = []
+
+    def work(i):
+        try:
+            for _ in range(3):
+                f, psf, op = jobs[i]
+                out[i] = rlDeconvolve(f, psf, RlConfig(iterations=15, op=op)).image
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(jobs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for a, b in zip(out, seq):
+        np.testing.assert_array_equal(a, b)
