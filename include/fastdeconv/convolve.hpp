@@ -15,8 +15,12 @@
 // numbers as with the CPU operators.
 #pragma once
 
+#include <cfloat>
+#include <cmath>
 #include <cstdint>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -61,16 +65,39 @@ inline void check(int status) {
     if (status != FDG_OK) raise(status);
 }
 
-/// Per-thread device context (device 0, private stream and scratch), created
-/// on first use: concurrent calls from different threads share nothing
-/// (the reference API is pure and reentrant).
-inline fdg_ctx* context() {
-    thread_local std::shared_ptr<fdg_ctx> ctx = [] {
+/// Per-thread device context on `device` (private stream, scratch and
+/// pinned staging), created on first use: concurrent calls from different
+/// threads share nothing (the reference API is pure and reentrant).
+inline fdg_ctx* context(int device) {
+    thread_local std::map<int, std::shared_ptr<fdg_ctx>> ctxs;
+    std::shared_ptr<fdg_ctx>& ctx = ctxs[device];
+    if (!ctx) {
         fdg_ctx* c = nullptr;
-        check(fdg_ctx_create(0, &c));
-        return std::shared_ptr<fdg_ctx>(c, fdg_ctx_destroy);
-    }();
+        check(fdg_ctx_create(device, &c));
+        ctx = std::shared_ptr<fdg_ctx>(c, fdg_ctx_destroy);
+    }
     return ctx.get();
+}
+
+/// ... on the calling thread's current CUDA device
+inline fdg_ctx* context() {
+    int device = 0;
+    check(fdg_get_device(&device));
+    return context(device);
+}
+
+/// rl.hpp:71-84's pixel checks on the caller's double values, before the
+/// fp32 conversion of the GPU path (a tiny negative would round to -0.0 and
+/// pass a check in fp32).  Finite values beyond the fp32 range cannot be
+/// represented on the device: refused with their own message.
+inline void validatePixels(const Image& f, const char* where) {
+    for (double v : f.data()) {
+        if (!std::isfinite(v)) throw std::invalid_argument(std::string(where) + ": input image has non-finite pixels");
+        if (v < 0.0) throw std::invalid_argument(std::string(where) + ": input image must be nonnegative");
+    }
+    for (double v : f.data())
+        if (v > static_cast<double>(FLT_MAX))
+            throw std::invalid_argument(std::string(where) + ": input pixel exceeds the fp32 range of the GPU path");
 }
 
 /// fdg_psf_desc view of a reference Psf (owns the flattened arrays).
@@ -174,27 +201,39 @@ inline OperatorKind dispatch(const Psf& psf, OperatorKind preference = OperatorK
 }
 
 /// A PSF bound to its resolved operator and its device-resident
-/// representation (convolve.hpp:650-753).  Immutable; applications are
-/// serialised on the shared GPU context.
+/// representation (convolve.hpp:650-753).  Construction is host-only like the
+/// reference's (dispatch); the device representation is built on first use
+/// on the calling thread's current device and is immutable afterwards, so
+/// copies and concurrent applications from several threads (each on its
+/// own context) are safe.
 class ConvPlan {
 public:
     explicit ConvPlan(const Psf& psf, OperatorKind preference = OperatorKind::Auto)
-        : kind_(dispatch(psf, preference)), psf_(psf) {
-        fdg_plan* p = nullptr;
-        gpu_detail::check(fdg_plan_create(gpu_detail::context(), gpu_detail::Desc(psf).get(),
-                                          static_cast<int>(kind_), &p));
-        plan_ = std::shared_ptr<fdg_plan>(p, fdg_plan_destroy);
-    }
+        : kind_(dispatch(psf, preference)), psf_(psf), state_(std::make_shared<State>()) {}
 
     OperatorKind kind() const { return kind_; }
-    /// the PSF the plan was built from (the GPU RL step re-derives the adjoint)
+    /// the PSF the plan was built from
     const Psf& psf() const { return psf_; }
+
+    /// the device plan (libfdgpu handle), built once
+    fdg_plan* native() const {
+        std::call_once(state_->once, [this] {
+            fdg_plan* p = nullptr;
+            gpu_detail::check(fdg_plan_create(gpu_detail::context(), gpu_detail::Desc(psf_).get(),
+                                              static_cast<int>(kind_), &p));
+            state_->plan = std::shared_ptr<fdg_plan>(p, fdg_plan_destroy);
+        });
+        return state_->plan.get();
+    }
+
+    /// the calling thread's context on the plan's device
+    fdg_ctx* callerContext() const { return gpu_detail::context(fdg_plan_device(native())); }
 
     void applyInto(const Image& img, ConvWorkspace&, Image& out, ConvCounters* counters = nullptr) const {
         const int w = img.width(), h = img.height();
         const std::vector<float> in = gpu_detail::toFloat(img);
         std::vector<float> res(in.size());
-        gpu_detail::check(fdg_conv_apply(plan_.get(), in.data(), w, h, res.data()));
+        gpu_detail::check(fdg_conv_apply_ctx(callerContext(), native(), in.data(), w, h, res.data()));
         out = gpu_detail::fromFloat(res, w, h);
         addCounters(counters, w, h);
     }
@@ -216,11 +255,12 @@ public:
         const int w = img.width(), h = img.height();
         const std::vector<float> in = gpu_detail::toFloat(img), fb = gpu_detail::toFloat(fallback);
         std::vector<float> res(in.size());
-        gpu_detail::check(fdg_conv_apply_masked(plan_.get(), in.data(), w, h, active.data(), fb.data(), res.data()));
+        gpu_detail::check(fdg_conv_apply_masked_ctx(callerContext(), native(), in.data(), w, h, active.data(),
+                                                    fb.data(), res.data()));
         out = gpu_detail::fromFloat(res, w, h);
         if (counters) {
             std::uint64_t c[3];
-            gpu_detail::check(fdg_plan_counters(plan_.get(), w, h, c));
+            gpu_detail::check(fdg_op_counters(gpu_detail::Desc(psf_).get(), static_cast<int>(kind_), w, h, c));
             std::uint64_t visited = 0;
             for (std::uint8_t a : active) visited += a != 0;
             const std::uint64_t n = static_cast<std::uint64_t>(w) * h;
@@ -238,13 +278,18 @@ public:
     }
 
     /// the device engine serving this plan ("box", "taps", "dense", ...)
-    std::string engine() const { return fdg_plan_engine(plan_.get()); }
+    std::string engine() const { return fdg_plan_engine(native()); }
 
 private:
+    struct State {
+        std::once_flag once;
+        std::shared_ptr<fdg_plan> plan;
+    };
+
     void addCounters(ConvCounters* counters, int w, int h) const {
         if (!counters) return;
         std::uint64_t c[3];
-        gpu_detail::check(fdg_plan_counters(plan_.get(), w, h, c));
+        gpu_detail::check(fdg_op_counters(gpu_detail::Desc(psf_).get(), static_cast<int>(kind_), w, h, c));
         counters->pixels += c[0];
         counters->perPixelOps += c[1];
         counters->setupOps += c[2];
@@ -252,7 +297,7 @@ private:
 
     OperatorKind kind_;
     Psf psf_;
-    std::shared_ptr<fdg_plan> plan_;
+    std::shared_ptr<State> state_;  // shared by copies: one device plan
 };
 
 inline Image convolve(const Image& img, const Psf& psf, OperatorKind kind = OperatorKind::Auto,

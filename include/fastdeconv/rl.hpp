@@ -85,6 +85,14 @@ inline RlTrace toTrace(const std::vector<fdg_rl_record>& recs) {
 /// still runs in the library; compute then reports the missing device)
 inline fdg_ctx* contextOrNull() { return fdg_device_available() ? context() : nullptr; }
 
+/// rl.hpp:71-84 in the reference's order (config, then pixels in double)
+inline void validateRlInputs(const Image& f, const RlConfig& cfg, const char* where) {
+    if (f.empty()) throw std::invalid_argument(std::string(where) + ": empty input image");
+    if (cfg.iterations < 0) throw std::invalid_argument(std::string(where) + ": iterations must be >= 0");
+    if (!(cfg.epsilonDiv > 0.0)) throw std::invalid_argument(std::string(where) + ": epsilonDiv must be positive");
+    validatePixels(f, where);
+}
+
 }  // namespace gpu_detail
 
 
@@ -102,7 +110,7 @@ inline Image rlStep(const Image& u, const Image& f, const Psf& h, const RlConfig
 
 /// rl.hpp:140-179
 inline RlResult rlDeconvolve(const Image& f, const Psf& h, const RlConfig& cfg = {}) {
-    if (f.empty()) throw std::invalid_argument("rlDeconvolve: empty input image");
+    gpu_detail::validateRlInputs(f, cfg, "rlDeconvolve");
     const std::vector<float> ff = gpu_detail::toFloat(f);
     std::vector<float> u(ff.size());
     std::vector<fdg_rl_record> recs(static_cast<size_t>(cfg.iterations > 0 ? cfg.iterations : 0));
@@ -115,7 +123,7 @@ inline RlResult rlDeconvolve(const Image& f, const Psf& h, const RlConfig& cfg =
 /// rl.hpp:187-257 (+ thinStart, see the header comment)
 inline RlResult rlDeconvolveSelective(const Image& f, const Psf& h, const RlConfig& cfg, double threshold,
                                       int period = 10, int thinStart = 0) {
-    if (f.empty()) throw std::invalid_argument("rlDeconvolveSelective: empty input image");
+    gpu_detail::validateRlInputs(f, cfg, "rlDeconvolveSelective");
     const std::vector<float> ff = gpu_detail::toFloat(f);
     std::vector<float> u(ff.size());
     std::vector<fdg_rl_record> recs(static_cast<size_t>(cfg.iterations > 0 ? cfg.iterations : 0));
@@ -133,18 +141,17 @@ inline Image blurImage(const Image& g, const Psf& h, BoundaryMode mode) {
 }
 
 namespace detail {
-/// rlStepPlanned (rl.hpp:101-125): one step with the forward plan's operator;
-/// the device derives ConvPlan(adjoint(h), forward.kind()) itself.
-inline Image rlStepPlanned(const Image& u, const Image& f, const ConvPlan& forward, const ConvPlan& /*adjoint*/,
+/// rlStepPlanned (rl.hpp:101-125): one step with the caller's forward and
+/// adjoint plans (their device representations, applied on the calling
+/// thread's context).
+inline Image rlStepPlanned(const Image& u, const Image& f, const ConvPlan& forward, const ConvPlan& adjointPlan,
                            const RlConfig& cfg, double* maxAbsChange = nullptr) {
-    RlConfig c = cfg;
-    c.op = forward.kind();
     const std::vector<float> uf = gpu_detail::toFloat(u), ff = gpu_detail::toFloat(f);
     std::vector<float> out(uf.size());
-    const fdg_rl_config cc = gpu_detail::toC(c);
+    const fdg_rl_config cc = gpu_detail::toC(cfg);
     double mc = 0.0;
-    gpu_detail::check(fdg_rl_step(gpu_detail::contextOrNull(), gpu_detail::Desc(forward.psf()).get(), &cc, uf.data(),
-                                  ff.data(), u.width(), u.height(), out.data(), &mc));
+    gpu_detail::check(fdg_rl_step_planned(forward.callerContext(), forward.native(), adjointPlan.native(), &cc,
+                                          uf.data(), ff.data(), u.width(), u.height(), out.data(), &mc));
     if (maxAbsChange) *maxAbsChange = mc;
     return gpu_detail::fromFloat(out, u.width(), u.height());
 }

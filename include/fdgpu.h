@@ -92,6 +92,8 @@ int fdg_abi_version(void);
 const char* fdg_last_error(void);
 /* 1 when a CUDA device is usable, else 0 */
 int fdg_device_available(void);
+/* the calling thread's current CUDA device (FDG_ECUDA without a device) */
+int fdg_get_device(int* device);
 /* Process-wide engine options (no reference counterpart; tuning/testing):
  *   "fused": 1 = run each RL iteration of the centred 15x15 box as one fused
  *            pass (kernels_fused.cu, default), 0 = two fused-epilogue passes.
@@ -101,7 +103,13 @@ int fdg_device_available(void);
  * Returns the previous value, or -1 for an unknown name. */
 int fdg_set_option(const char* name, int value);
 
-/* Context: device, stream (default: a private non-blocking stream). */
+/* Context: device, stream (default: a private non-blocking stream), scratch
+ * and pinned staging buffers.  Calls on one context are serialised (one
+ * caller at a time); calls on different contexts share nothing, so a
+ * per-thread context makes the API reentrant like the reference
+ * (SPEC.md:314).  Every entry point runs on the context's device and
+ * restores the caller's current device.  fdg_ctx_destroy drops the caller's
+ * reference: plans and solvers created on the context keep it alive. */
 int fdg_ctx_create(int device, fdg_ctx** out);
 void fdg_ctx_destroy(fdg_ctx* ctx);
 /* run on an external cudaStream_t (e.g. torch.cuda.current_stream()) */
@@ -116,7 +124,9 @@ int fdg_dispatch(const fdg_psf_desc* psf, int preference, int* kind);
 /* operatorAcceptsPsf(), convolve.hpp:607-625 */
 int fdg_operator_accepts(int kind, const fdg_psf_desc* psf, int* accepts);
 
-/* ConvPlan(psf, preference), convolve.hpp:652-676 */
+/* ConvPlan(psf, preference), convolve.hpp:652-676.  The plan holds the
+ * device representation (uploaded on ctx's device) and is immutable: any
+ * context on that device may apply it concurrently (fdg_conv_apply_ctx). */
 int fdg_plan_create(fdg_ctx* ctx, const fdg_psf_desc* psf, int preference, fdg_plan** out);
 void fdg_plan_destroy(fdg_plan* plan);
 /* ConvPlan::kind(), convolve.hpp:678 */
@@ -131,11 +141,18 @@ int fdg_op_counters(const fdg_psf_desc* psf, int preference, int width, int heig
 /* which device engine serves the plan: "rows", "box2d", "spans", "dense",
  * "taps" or "cyclic" (diagnostics / bench labels) */
 const char* fdg_plan_engine(const fdg_plan* plan);
+/* CUDA device the plan's representation lives on */
+int fdg_plan_device(const fdg_plan* plan);
 
-/* ConvPlan::applyInto, convolve.hpp:680-715 (host buffers) */
+/* ConvPlan::applyInto, convolve.hpp:680-715 (host buffers), on the calling
+ * thread's context `ctx` (scratch, stream); fdg_conv_apply uses the context
+ * the plan was created on. */
+int fdg_conv_apply_ctx(fdg_ctx* ctx, const fdg_plan* plan, const float* in, int width, int height, float* out);
 int fdg_conv_apply(fdg_plan* plan, const float* in, int width, int height, float* out);
 /* ConvPlan::applyMaskedInto, convolve.hpp:724-736: only Naive and List plans,
  * else FDG_EINVAL "operator does not support masked evaluation" */
+int fdg_conv_apply_masked_ctx(fdg_ctx* ctx, const fdg_plan* plan, const float* in, int width, int height,
+                              const uint8_t* active, const float* fallback, float* out);
 int fdg_conv_apply_masked(fdg_plan* plan, const float* in, int width, int height,
                           const uint8_t* active, const float* fallback, float* out);
 /* device-resident variant on the context stream */
@@ -143,7 +160,10 @@ int fdg_conv_apply_device(fdg_plan* plan, const float* d_in, float* d_out, int w
                           int pitch);
 
 /* ---- Richardson-Lucy drivers (host buffers) ------------------------- */
-/* rlDeconvolve, rl.hpp:140-179.  trace: nullable, cfg->iterations records */
+/* rlDeconvolve, rl.hpp:140-179.  trace: nullable, cfg->iterations records;
+ * seconds = per-iteration device time (%globaltimer stamps written by each
+ * iteration's last kernel, so graph-replayed loops report real per-iteration
+ * times) */
 int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg,
                       const float* f, int width, int height, float* u_out, fdg_rl_record* trace);
 /* rlDeconvolveSelective, rl.hpp:187-257.  thin_start: deactivation is held
@@ -158,6 +178,11 @@ int fdg_rl_deconvolve_selective(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg
 /* rlStep, rl.hpp:131-137 */
 int fdg_rl_step(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg, const float* u,
                 const float* f, int width, int height, float* u_out, double* max_abs_change);
+/* detail::rlStepPlanned, rl.hpp:101-125: one step with the caller's forward
+ * and adjoint plans (both on ctx's device) */
+int fdg_rl_step_planned(fdg_ctx* ctx, const fdg_plan* forward, const fdg_plan* adjoint, const fdg_rl_config* cfg,
+                        const float* u, const float* f, int width, int height, float* u_out,
+                        double* max_abs_change);
 
 /* ---- device-resident solver (bench, sharding, batches) --------------- */
 /* Plans for h and adjoint(h) + per-iteration trace arrays, for `batch`
@@ -186,7 +211,8 @@ int fdg_solver_pass(fdg_solver* s, int pass, const float* d_in, const float* d_a
  * u_in != u_out. */
 int fdg_solver_iterate(fdg_solver* s, const float* d_f, const float* d_u_in, float* d_u_out, int pitch,
                        long long image_stride, int y0, int y1, int ylo, int yhi, int iteration);
-/* copy per-iteration {max|du|, NaN} back (synchronises) */
+/* copy per-iteration {max|du|, NaN (in inactive_fraction), seconds} of the
+ * last run back (synchronises) */
 int fdg_solver_trace(fdg_solver* s, fdg_rl_record* out, int n);
 /* Engine fdg_solver_run uses: "fused" (one launch per iteration), "rowres"
  * (one launch per run) or the plan engine of the two-pass loop ("box",

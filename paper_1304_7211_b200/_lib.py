@@ -94,6 +94,11 @@ def lib():
             "fdg_abi_version": (C.c_int, []),
             "fdg_last_error": (C.c_char_p, []),
             "fdg_device_available": (C.c_int, []),
+            "fdg_get_device": (C.c_int, [ip]),
+            "fdg_plan_device": (C.c_int, [vp]),
+            "fdg_conv_apply_ctx": (C.c_int, [vp, vp, fp, C.c_int, C.c_int, fp]),
+            "fdg_conv_apply_masked_ctx": (C.c_int, [vp, vp, fp, C.c_int, C.c_int, u8p, fp, fp]),
+            "fdg_rl_step_planned": (C.c_int, [vp, vp, vp, C.POINTER(RlConfigC), fp, fp, C.c_int, C.c_int, fp, dp]),
             "fdg_set_option": (C.c_int, [C.c_char_p, C.c_int]),
             "fdg_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
             "fdg_ctx_destroy": (None, [vp]),
@@ -215,7 +220,11 @@ class Context:
         return cls.default().h
 
     @classmethod
-    def default(cls, device: int = 0) -> "Context":
+    def default(cls, device: int = None) -> "Context":
+        """The calling thread's context on `device` (default: the thread's
+        current CUDA device)."""
+        if device is None:
+            device = current_device()
         per_thread = getattr(cls._tls, "ctx", None)
         if per_thread is None:
             per_thread = cls._tls.ctx = {}
@@ -239,6 +248,38 @@ class Context:
                 lib().fdg_ctx_destroy(self.h)
         except Exception:
             pass
+
+
+def current_device() -> int:
+    """The calling thread's current CUDA device (0 when none is usable)."""
+    d = C.c_int(0)
+    if lib().fdg_get_device(C.byref(d)) != FDG_OK:
+        return 0
+    return d.value
+
+
+_FLT_MAX = float(np.finfo(np.float32).max)
+
+
+def validate_image(a: np.ndarray, where: str):
+    """rl.hpp:78-83 on the caller's own values (before the fp32 conversion of
+    the GPU path): the first non-finite or negative pixel in row-major order
+    decides the message (non-finite first at the same pixel).  Finite values
+    beyond the fp32 range cannot be represented on the device and are
+    refused with their own message (the reference would accept them)."""
+    if a.dtype == np.float32 or a.size == 0:
+        return  # exactly what the device sees; validated there
+    v = np.asarray(a, dtype=np.float64).ravel()
+    bad_nf = np.flatnonzero(~np.isfinite(v))
+    bad_neg = np.flatnonzero(v < 0)
+    i_nf = bad_nf[0] if bad_nf.size else None
+    i_neg = bad_neg[0] if bad_neg.size else None
+    if i_nf is not None and (i_neg is None or i_nf <= i_neg):
+        raise FdgInvalidArgument(f"{where}: input image has non-finite pixels")
+    if i_neg is not None:
+        raise FdgInvalidArgument(f"{where}: input image must be nonnegative")
+    if v.size and float(v.max()) > _FLT_MAX:
+        raise FdgInvalidArgument(f"{where}: input pixel exceeds the fp32 range of the GPU path")
 
 
 def f32(a) -> np.ndarray:

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import threading
 from dataclasses import dataclass
 from typing import Optional
 
@@ -109,21 +110,35 @@ class ConvPlan:
 
     def __init__(self, psf, preference=OperatorKind.Auto, ctx: Optional[Context] = None):
         self._psf = psf
-        self._kind = dispatch(psf, preference)
-        self._ctx = ctx
+        self._kind = dispatch(psf, preference)  # host-only: no device needed
+        self._ctx = ctx      # explicit context (else: the calling thread's)
+        self._home = None    # context the device representation was built on
         self._h = None
+        self._lock = threading.Lock()
 
     def kind(self) -> OperatorKind:
         return self._kind
 
     def _plan(self):
+        """The immutable device plan (built once, on first use)."""
         if self._h is None:
-            ctx = self._ctx or Context.default()
-            h = C.c_void_p()
-            d = Desc(self._psf)
-            check(lib().fdg_plan_create(ctx.h, d.ref, int(self._kind), C.byref(h)))
-            self._ctx, self._h = ctx, h
+            with self._lock:
+                if self._h is None:
+                    ctx = self._ctx or Context.default()
+                    h = C.c_void_p()
+                    d = Desc(self._psf)
+                    check(lib().fdg_plan_create(ctx.h, d.ref, int(self._kind), C.byref(h)))
+                    self._home, self._h = ctx, h
         return self._h
+
+    def _caller_ctx(self):
+        """Scratch and stream of this call: the explicit context, else the
+        calling thread's default context on the plan's device (concurrent
+        applications from several threads share nothing but the plan)."""
+        plan = self._plan()
+        if self._ctx is not None:
+            return self._ctx.h, plan
+        return Context.default(lib().fdg_plan_device(plan)).h, plan
 
     def engine(self) -> str:
         return lib().fdg_plan_engine(self._plan()).decode()
@@ -141,7 +156,8 @@ class ConvPlan:
         src = f32(a)
         out = np.empty_like(src)
         h, w = src.shape
-        check(lib().fdg_conv_apply(self._plan(), fptr(src), w, h, fptr(out)))
+        ctx, plan = self._caller_ctx()
+        check(lib().fdg_conv_apply_ctx(ctx, plan, fptr(src), w, h, fptr(out)))
         self._count(counters, w, h)
         return out.astype(_out_dtype(a), copy=False)
 
@@ -162,8 +178,9 @@ class ConvPlan:
         src, fb32 = f32(a), f32(fb)
         out = np.empty_like(src)
         h, w = src.shape
-        check(lib().fdg_conv_apply_masked(self._plan(), fptr(src), w, h, u8ptr(act.reshape(h, w)),
-                                          fptr(fb32), fptr(out)))
+        ctx, plan = self._caller_ctx()
+        check(lib().fdg_conv_apply_masked_ctx(ctx, plan, fptr(src), w, h, u8ptr(act.reshape(h, w)),
+                                              fptr(fb32), fptr(out)))
         if counters is not None:
             c = np.zeros(3, dtype=np.uint64)
             check(lib().fdg_op_counters(Desc(self._psf).ref, int(self._kind), w, h,

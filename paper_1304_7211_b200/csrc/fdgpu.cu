@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <chrono>
@@ -72,25 +73,96 @@ int pitch_for(int W) { return (W % 4 == 0) ? W : ((W + 31) & ~31); }
 
 }  // namespace
 
+namespace {
+// ---- host <-> device copies.  Pinned (or registered) host memory goes
+// straight to the DMA engines.  Pageable memory is staged through two pinned
+// chunks: the DMA of one chunk overlaps a multi-threaded (OpenMP) memcpy of
+// the other, instead of the driver's single-threaded pageable path (measured
+// 4.7 GB/s for a 1 GiB D2H into a fresh numpy array on the B200 host).  One
+// staging pair per context: calls on different contexts (threads) never
+// share a chunk, and a context's calls are serialised by its mutex.
+struct Staging {
+    static constexpr size_t CHUNK = 32u << 20;
+    float* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaError_t init() {
+        if (buf[0]) return cudaSuccess;
+        for (int i = 0; i < 2; ++i) {
+            cudaError_t e = cudaHostAlloc(&buf[i], CHUNK, cudaHostAllocDefault);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
+    ~Staging() {
+        for (int i = 0; i < 2; ++i) {
+            if (ev[i]) cudaEventSynchronize(ev[i]), cudaEventDestroy(ev[i]);
+            if (buf[i]) cudaFreeHost(buf[i]);
+        }
+    }
+};
+
+// Selects a device for the duration of an entry point and restores the
+// caller's current device afterwards (torch and other libraries keep their
+// own notion of the current device).
+struct DevScope {
+    int prev = -1;
+    cudaError_t enter(int dev) {
+        cudaError_t e = cudaGetDevice(&prev);
+        if (e != cudaSuccess) {
+            prev = -1;
+            return e;
+        }
+        if (prev == dev) {
+            prev = -1;
+            return cudaSuccess;
+        }
+        return cudaSetDevice(dev);
+    }
+    ~DevScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+}  // namespace
+
 struct fdg_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     uint64_t launches = 0;
+    // one caller at a time per context (scratch, staging, stream, cached
+    // solver); recursive: entry points call each other
+    std::recursive_mutex mu;
+    // plans and solvers created through the ABI keep their context alive
+    std::atomic<int> refs{1};
+    Staging stg;
     // scratch for the host-buffer entry points (kept across calls)
     DevBuf<float> a, b, c, d;
     DevBuf<uint8_t> m;
     DevBuf<unsigned> tr_max;
     DevBuf<int> tr_nan;
-    DevBuf<unsigned long long> tr_inact, first_bad;
+    DevBuf<unsigned long long> tr_inact, first_bad, tr_time;
+    // masked dense passes: compacted active-block lists per 64x64 tile
+    DevBuf<int> tile_blocks, tile_count;
     // rlDeconvolve on host buffers keeps the last call's solver (plans + the
     // captured CUDA graph of the iteration loop) keyed by PSF, config and size
     fdg_solver* rl_solver = nullptr;
     std::string rl_key;
+    ~fdg_ctx();
 };
 
+namespace {
+void ctx_retain(fdg_ctx* c) {
+    if (c) c->refs.fetch_add(1, std::memory_order_relaxed);
+}
+void ctx_release(fdg_ctx* c) {
+    if (c && c->refs.fetch_sub(1, std::memory_order_acq_rel) == 1) delete c;
+}
+}  // namespace
+
 struct fdg_plan {
-    fdg_ctx* ctx = nullptr;
+    fdg_ctx* ctx = nullptr;  // device (and uploads) of the plan
+    bool holds_ref = false;  // created through fdg_plan_create: keeps ctx alive
     int kind = FDG_OP_NAIVE;
     HostPsf psf;  // the representation the plan stores (ConvPlan members)
     LineShape line{};
@@ -99,18 +171,20 @@ struct fdg_plan {
     std::vector<Tap> taps;  // list / naive tap view
     DevPsf dev;
     int wrap = 0;
-    // masked dense path: compacted per-tile block lists
-    DevBuf<int> tile_blocks, tile_count;
     ~fdg_plan() {
+        DevScope ds;
+        if (ctx) ds.enter(ctx->device);
         cudaFree(dev.d_row_start);
         cudaFree(dev.d_dx);
         cudaFree(dev.d_w);
         cudaFree(dev.d_dense);
+        if (holds_ref) ctx_release(ctx);
     }
 };
 
 struct fdg_solver {
     fdg_ctx* ctx = nullptr;
+    bool holds_ref = false;  // created through fdg_solver_create: keeps ctx alive
     std::unique_ptr<fdg_plan> fwd, adj;
     fdg_rl_config cfg{};
     int W = 0, H = 0, batch = 1;
@@ -118,8 +192,12 @@ struct fdg_solver {
     DevBuf<float> q;
     DevBuf<unsigned> maxchange;
     DevBuf<int> nanflag;
-    // CUDA graph of one full fdg_solver_run (replayed while the arguments match)
+    // %globaltimer stamps: [0] start of the last run, [k + 1] end of iteration k
+    DevBuf<unsigned long long> tstamp;
+    // CUDA graph of one full fdg_solver_run (replayed while the arguments and
+    // the engine options it was captured under match)
     cudaGraphExec_t gexec = nullptr;
+    int g_opts = -1;
     const void* g_f = nullptr;
     const void* g_u = nullptr;
     int g_pitch = 0, g_iters = -1;
@@ -130,12 +208,32 @@ struct fdg_solver {
     cudaStream_t gstream = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     ~fdg_solver() {
+        DevScope ds;
+        if (ctx) ds.enter(ctx->device);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (ev_in) cudaEventDestroy(ev_in);
         if (ev_out) cudaEventDestroy(ev_out);
         if (gstream) cudaStreamDestroy(gstream);
+        fwd.reset();
+        adj.reset();
+        maxchange.release();
+        nanflag.release();
+        tstamp.release();
+        q.release();
+        if (holds_ref) ctx_release(ctx);
     }
 };
+
+fdg_ctx::~fdg_ctx() {
+    DevScope ds;
+    ds.enter(device);
+    if (stream) cudaStreamSynchronize(stream);
+    fdg_solver_destroy(rl_solver);
+    if (own_stream) cudaStreamDestroy(stream);
+    a.release(), b.release(), c.release(), d.release(), m.release();
+    tr_max.release(), tr_nan.release(), tr_inact.release(), first_bad.release(), tr_time.release();
+    tile_blocks.release(), tile_count.release();
+}
 
 namespace {
 
@@ -326,8 +424,8 @@ int build_plan(fdg_ctx* ctx, const HostPsf& psf, int preference, std::unique_ptr
     return FDG_OK;
 }
 
-// One fused pass of `pl` over geometry g with epilogue e.
-int run_pass(fdg_plan* pl, const Geom& g, const Epi& e, cudaStream_t st) {
+// One fused pass of `pl` over geometry g with epilogue e, on ctx's scratch.
+int run_pass(fdg_ctx* ctx, const fdg_plan* pl, const Geom& g, const Epi& e, cudaStream_t st) {
     cudaError_t r = cudaSuccess;
     const DevPsf& d = pl->dev;
     const bool masked = e.active != nullptr;
@@ -344,13 +442,13 @@ int run_pass(fdg_plan* pl, const Geom& g, const Epi& e, cudaStream_t st) {
             if (masked) {
                 const DenseTiling t = dense_tiling(g.W, g.y1 - g.y0);
                 const size_t tiles = (size_t)t.tiles_x * t.tiles_y;
-                if ((r = pl->tile_blocks.ensure(tiles * 256)) != cudaSuccess) break;
-                if ((r = pl->tile_count.ensure(tiles)) != cudaSuccess) break;
+                if ((r = ctx->tile_blocks.ensure(tiles * 256)) != cudaSuccess) break;
+                if ((r = ctx->tile_count.ensure(tiles)) != cudaSuccess) break;
                 if (g.batch != 1 || g.y0 != 0) return set_err(FDG_EINVAL, "masked dense pass: single image only");
-                r = launch_tile_compact(e.active, g.W, g.y1, g.pitch, pl->tile_blocks.p, pl->tile_count.p,
+                r = launch_tile_compact(e.active, g.W, g.y1, g.pitch, ctx->tile_blocks.p, ctx->tile_count.p,
                                         nullptr, st);
-                if (r == cudaSuccess) r = launch_dense(d, g, e, st, pl->tile_blocks.p, pl->tile_count.p);
-                pl->ctx->launches += 1;
+                if (r == cudaSuccess) r = launch_dense(d, g, e, st, ctx->tile_blocks.p, ctx->tile_count.p);
+                ctx->launches += 1;
             } else {
                 r = launch_dense(d, g, e, st, nullptr, nullptr);
             }
@@ -364,7 +462,7 @@ int run_pass(fdg_plan* pl, const Geom& g, const Epi& e, cudaStream_t st) {
         }
     }
     if (r != cudaSuccess) return cuda_err(r, "kernel launch");
-    pl->ctx->launches += 1;
+    ctx->launches += 1;
     return FDG_OK;
 }
 
@@ -376,13 +474,26 @@ bool use_rowres(const fdg_plan* pl, int W) {
     return !off && d.engine == ENG_RECT && rowres_supported(d.mx, d.my, d.min_dx, d.min_dy, W);
 }
 
-int run_rowres(fdg_plan* pl, const float* f, float* u, int pitch, int W, int H, int batch, long long bstride,
-               int iters, const fdg_rl_config* cfg, unsigned* mc, int* nf, cudaStream_t st) {
+// Trace slots of a loop of `iters` iterations: per-iteration max|du| (float
+// bits), NaN flag, and %globaltimer stamps ([0] = start, [k + 1] = end of
+// iteration k).  Any pointer may be null.
+struct TraceSlots {
+    unsigned* mc = nullptr;
+    int* nf = nullptr;
+    unsigned long long* ts = nullptr;
+    unsigned* mc_at(int k) const { return mc ? mc + k : nullptr; }
+    int* nf_at(int k) const { return nf ? nf + k : nullptr; }
+    unsigned long long* end_at(int k) const { return ts ? ts + 1 + k : nullptr; }
+};
+
+int run_rowres(fdg_ctx* ctx, const fdg_plan* pl, const float* f, float* u, int pitch, int W, int H, int batch,
+               long long bstride, int iters, const fdg_rl_config* cfg, const TraceSlots& tr, cudaStream_t st) {
     const DevPsf& d = pl->dev;
     cudaError_t r = launch_rowres(d.mx, d.min_dx, d.scale, f, u, pitch, W, H, batch, bstride, iters,
-                                  (float)cfg->epsilon_div, cfg->clamp_nonnegative, mc, nf, st);
+                                  (float)cfg->epsilon_div, cfg->clamp_nonnegative, tr.mc, tr.nf, tr.end_at(0), tr.ts,
+                                  st);
     if (r != cudaSuccess) return cuda_err(r, "row-resident RL launch");
-    pl->ctx->launches += 1;
+    ctx->launches += 1;
     return FDG_OK;
 }
 
@@ -393,15 +504,15 @@ bool use_fused(const fdg_plan* pl) {
     return d.engine == ENG_RECT && fused_supported(d.mx, d.my, d.min_dx, d.min_dy);
 }
 
-int run_fused(fdg_plan* pl, const float* u_in, const float* f, float* u_out, int pitch, int W, int H, int batch,
-              long long bstride, const fdg_rl_config* cfg, unsigned* mc, int* nf, cudaStream_t st, int y0 = 0,
-              int y1 = -1, int ylo = 0, int yhi = -1) {
+int run_fused(fdg_ctx* ctx, const fdg_plan* pl, const float* u_in, const float* f, float* u_out, int pitch, int W,
+              int H, int batch, long long bstride, const fdg_rl_config* cfg, unsigned* mc, int* nf,
+              unsigned long long* te, cudaStream_t st, int y0 = 0, int y1 = -1, int ylo = 0, int yhi = -1) {
     if (y1 < 0) y1 = H;
     if (yhi < 0) yhi = H - 1;
     cudaError_t r = launch_fused(u_in, f, u_out, pitch, W, y0, y1, ylo, yhi, batch, bstride, pl->dev.scale,
-                                 (float)cfg->epsilon_div, cfg->clamp_nonnegative, mc, nf, st);
+                                 (float)cfg->epsilon_div, cfg->clamp_nonnegative, mc, nf, te, st);
     if (r != cudaSuccess) return cuda_err(r, "fused RL iteration launch");
-    pl->ctx->launches += 1;
+    ctx->launches += 1;
     return FDG_OK;
 }
 
@@ -420,36 +531,23 @@ Geom whole(const float* in, float* out, int pitch, int W, int H, int batch = 1, 
     return g;
 }
 
-int check_device(fdg_ctx* ctx) {
+// Every device entry point holds its context's lock and runs on the
+// context's device (the caller's current device is restored on return).
+struct Entry {
+    std::unique_lock<std::recursive_mutex> lk;
+    DevScope ds;  // destroyed first: the device is restored before unlocking
+};
+
+int enter(fdg_ctx* ctx, Entry& en) {
     if (!ctx) return set_err(FDG_ECUDA, "no CUDA context (no device available; the B200 path has no CPU fallback)");
-    CK(cudaSetDevice(ctx->device));
+    en.lk = std::unique_lock<std::recursive_mutex>(ctx->mu);
+    cudaError_t e = en.ds.enter(ctx->device);
+    if (e != cudaSuccess) return cuda_err(e, "cudaSetDevice");
     return FDG_OK;
 }
 
-// ---- host <-> device copies.  Pinned (or registered) host memory goes
-// straight to the DMA engines.  Pageable memory is staged through two pinned
-// chunks: the DMA of one chunk overlaps a multi-threaded (OpenMP) memcpy of
-// the other, instead of the driver's single-threaded pageable path (measured
-// 4.7 GB/s for a 1 GiB D2H into a fresh numpy array on the B200 host).
-struct Staging {
-    static constexpr size_t CHUNK = 32u << 20;
-    std::mutex mu;
-    float* buf[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    cudaError_t init() {
-        if (buf[0]) return cudaSuccess;
-        for (int i = 0; i < 2; ++i) {
-            cudaError_t e = cudaHostAlloc(&buf[i], CHUNK, cudaHostAllocDefault);
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
-            if (e != cudaSuccess) return e;
-        }
-        return cudaSuccess;
-    }
-};
-Staging& staging() {
-    static Staging* s = new Staging();  // process lifetime (pinned memory freed at exit)
-    return *s;
-}
+// engine options a captured graph depends on
+int options_key() { return fused_mode() * 16 + spans_mode(); }
 
 bool pageable(const void* p) {
     cudaPointerAttributes a;
@@ -478,14 +576,12 @@ void prefault(void* p, size_t bytes) {
     for (long long off = 0; off < (long long)bytes; off += page) c[off] = 0;
 }
 
-int h2d(float* d, int pitch, const float* h, int W, int H, cudaStream_t st) {
+int h2d(Staging& S, float* d, int pitch, const float* h, int W, int H, cudaStream_t st) {
     const size_t row = (size_t)W * 4;
     if (row * H < (4u << 20) || !pageable(h)) {
         CK(cudaMemcpy2DAsync(d, (size_t)pitch * 4, h, row, row, H, cudaMemcpyHostToDevice, st));
         return FDG_OK;
     }
-    Staging& S = staging();
-    std::lock_guard<std::mutex> lock(S.mu);
     CK(S.init());
     const int rows_per = (int)std::max<size_t>(1, Staging::CHUNK / row);
     for (int r0 = 0, k = 0; r0 < H; r0 += rows_per, k ^= 1) {
@@ -499,20 +595,21 @@ int h2d(float* d, int pitch, const float* h, int W, int H, cudaStream_t st) {
     return FDG_OK;
 }
 
-int d2h(float* h, const float* d, int pitch, int W, int H, cudaStream_t st) {
+int d2h(Staging& S, float* h, const float* d, int pitch, int W, int H, cudaStream_t st) {
     const size_t row = (size_t)W * 4;
     if (row * H < (4u << 20) || !pageable(h)) {
         CK(cudaMemcpy2DAsync(h, row, d, (size_t)pitch * 4, row, H, cudaMemcpyDeviceToHost, st));
         return FDG_OK;
     }
-    Staging& S = staging();
-    std::lock_guard<std::mutex> lock(S.mu);
     CK(S.init());
     const int rows_per = (int)std::max<size_t>(1, Staging::CHUNK / row);
     const int nchunk = (H + rows_per - 1) / rows_per;
     auto issue = [&](int c) -> cudaError_t {
         const int r0 = c * rows_per, nr = std::min(rows_per, H - r0);
-        cudaError_t e = cudaMemcpy2DAsync(S.buf[c & 1], row, d + (size_t)r0 * pitch, (size_t)pitch * 4, row, nr,
+        // the chunk's previous DMA (an h2d on another stream) has drained
+        cudaError_t e = cudaStreamWaitEvent(st, S.ev[c & 1], 0);
+        if (e != cudaSuccess) return e;
+        e = cudaMemcpy2DAsync(S.buf[c & 1], row, d + (size_t)r0 * pitch, (size_t)pitch * 4, row, nr,
                                           cudaMemcpyDeviceToHost, st);
         return e == cudaSuccess ? cudaEventRecord(S.ev[c & 1], st) : e;
     };
@@ -634,18 +731,33 @@ int fdg_device_available(void) {
     return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
 }
 
+int fdg_get_device(int* device) {
+    if (!device) return set_err(FDG_EINVAL, "null output");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return set_err(FDG_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    }
+    CK(cudaGetDevice(device));
+    return FDG_OK;
+}
+
 int fdg_ctx_create(int device, fdg_ctx** out) {
     if (!out) return set_err(FDG_EINVAL, "null output");
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
-    if (e != cudaSuccess || n == 0)
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
         return set_err(FDG_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    }
     if (device < 0 || device >= n) return set_err(FDG_EINVAL, "device index out of range");
-    CK(cudaSetDevice(device));
+    DevScope ds;
+    CK(ds.enter(device));
     auto* c = new fdg_ctx();
     c->device = device;
     e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
+        c->stream = nullptr;
         delete c;
         return cuda_err(e, "cudaStreamCreate");
     }
@@ -654,24 +766,27 @@ int fdg_ctx_create(int device, fdg_ctx** out) {
     return FDG_OK;
 }
 
-void fdg_ctx_destroy(fdg_ctx* ctx) {
-    if (!ctx) return;
-    cudaSetDevice(ctx->device);
-    fdg_solver_destroy(ctx->rl_solver);
-    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
-    delete ctx;
-}
+// Drops the caller's reference; plans and solvers created on the context
+// keep it alive until they are destroyed.
+void fdg_ctx_destroy(fdg_ctx* ctx) { ctx_release(ctx); }
 
 int fdg_ctx_set_stream(fdg_ctx* ctx, void* stream) {
-    if (!ctx) return set_err(FDG_EINVAL, "null context");
-    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    Entry en;
+    int st = enter(ctx, en);
+    if (st) return st;
+    if (ctx->own_stream && ctx->stream != (cudaStream_t)stream) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+    }
     ctx->stream = (cudaStream_t)stream;
     ctx->own_stream = false;
     return FDG_OK;
 }
 
 int fdg_ctx_synchronize(fdg_ctx* ctx) {
-    if (!ctx) return set_err(FDG_EINVAL, "null context");
+    Entry en;
+    int st = enter(ctx, en);
+    if (st) return st;
     CK(cudaStreamSynchronize(ctx->stream));
     return FDG_OK;
 }
@@ -697,14 +812,18 @@ int fdg_operator_accepts(int kind, const fdg_psf_desc* desc, int* accepts) {
 }
 
 int fdg_plan_create(fdg_ctx* ctx, const fdg_psf_desc* desc, int preference, fdg_plan** out) {
-    int st = check_device(ctx);
-    if (st) return st;
+    if (!out) return set_err(FDG_EINVAL, "null output");
     HostPsf h;
     std::string err;
     if (!psf_from_desc(desc, &h, &err)) return set_err(FDG_EINVAL, err);
+    Entry en;
+    int st = enter(ctx, en);
+    if (st) return st;
     std::unique_ptr<fdg_plan> pl;
     st = build_plan(ctx, h, preference, &pl);
     if (st) return st;
+    ctx_retain(ctx);
+    pl->holds_ref = true;
     *out = pl.release();
     return FDG_OK;
 }
@@ -712,6 +831,7 @@ int fdg_plan_create(fdg_ctx* ctx, const fdg_psf_desc* desc, int preference, fdg_
 void fdg_plan_destroy(fdg_plan* plan) { delete plan; }
 int fdg_plan_kind(const fdg_plan* plan) { return plan ? plan->kind : -1; }
 const char* fdg_plan_engine(const fdg_plan* plan) { return plan ? engine_name(plan->dev.engine) : "?"; }
+int fdg_plan_device(const fdg_plan* plan) { return plan && plan->ctx ? plan->ctx->device : -1; }
 
 }  // extern "C"
 
@@ -814,67 +934,95 @@ int fdg_op_counters(const fdg_psf_desc* desc, int preference, int W, int H, uint
 }
 }  // extern "C"
 
+namespace {
+// A plan serves the device it was built on.
+int check_plan_ctx(const fdg_ctx* ctx, const fdg_plan* pl) {
+    if (pl->ctx && ctx->device != pl->ctx->device)
+        return set_err(FDG_EINVAL, "ConvPlan belongs to CUDA device " + std::to_string(pl->ctx->device) +
+                                       ", the context to device " + std::to_string(ctx->device));
+    return FDG_OK;
+}
+}  // namespace
+
 extern "C" {
-int fdg_conv_apply(fdg_plan* pl, const float* in, int W, int H, float* out) {
+int fdg_conv_apply_ctx(fdg_ctx* ctx, const fdg_plan* pl, const float* in, int W, int H, float* out) {
     if (!pl || !in || !out) return set_err(FDG_EINVAL, "null argument");
     if (W < 1 || H < 1) return set_err(FDG_EINVAL, "Image: dimensions must be at least 1x1");
-    fdg_ctx* ctx = pl->ctx;
-    int st = check_device(ctx);
+    Entry en;
+    int st = enter(ctx, en);
     if (st) return st;
+    if ((st = check_plan_ctx(ctx, pl))) return st;
     const int pitch = pitch_for(W);
     const size_t n = (size_t)pitch * H;
     CK(ctx->a.ensure(n));
     CK(ctx->b.ensure(n));
-    if ((st = h2d(ctx->a.p, pitch, in, W, H, ctx->stream))) return st;
+    if ((st = h2d(ctx->stg, ctx->a.p, pitch, in, W, H, ctx->stream))) return st;
     Epi e;
     e.mode = EPI_STORE;
-    if ((st = run_pass(pl, whole(ctx->a.p, ctx->b.p, pitch, W, H), e, ctx->stream))) return st;
-    if ((st = d2h(out, ctx->b.p, pitch, W, H, ctx->stream))) return st;
+    if ((st = run_pass(ctx, pl, whole(ctx->a.p, ctx->b.p, pitch, W, H), e, ctx->stream))) return st;
+    if ((st = d2h(ctx->stg, out, ctx->b.p, pitch, W, H, ctx->stream))) return st;
     CK(cudaStreamSynchronize(ctx->stream));
     return FDG_OK;
+}
+
+int fdg_conv_apply(fdg_plan* pl, const float* in, int W, int H, float* out) {
+    return fdg_conv_apply_ctx(pl ? pl->ctx : nullptr, pl, in, W, H, out);
 }
 
 int fdg_conv_apply_device(fdg_plan* pl, const float* d_in, float* d_out, int W, int H, int pitch) {
     if (!pl || !d_in || !d_out) return set_err(FDG_EINVAL, "null argument");
     if (pitch % 4 || pitch < W) return set_err(FDG_EINVAL, "pitch must be a multiple of 4 and >= width");
+    Entry en;
+    int st = enter(pl->ctx, en);
+    if (st) return st;
     Epi e;
     e.mode = EPI_STORE;
-    return run_pass(pl, whole(d_in, d_out, pitch, W, H), e, pl->ctx->stream);
+    return run_pass(pl->ctx, pl, whole(d_in, d_out, pitch, W, H), e, pl->ctx->stream);
 }
 
-int fdg_conv_apply_masked(fdg_plan* pl, const float* in, int W, int H, const uint8_t* active,
-                          const float* fallback, float* out) {
+int fdg_conv_apply_masked_ctx(fdg_ctx* ctx, const fdg_plan* pl, const float* in, int W, int H,
+                              const uint8_t* active, const float* fallback, float* out) {
     if (!pl || !in || !out || !active || !fallback) return set_err(FDG_EINVAL, "null argument");
     if (pl->kind != FDG_OP_NAIVE && pl->kind != FDG_OP_LIST)
         return set_err(FDG_EINVAL, "operator does not support masked evaluation");
-    fdg_ctx* ctx = pl->ctx;
-    int st = check_device(ctx);
+    if (W < 1 || H < 1) return set_err(FDG_EINVAL, "Image: dimensions must be at least 1x1");
+    Entry en;
+    int st = enter(ctx, en);
     if (st) return st;
+    if ((st = check_plan_ctx(ctx, pl))) return st;
     const int pitch = pitch_for(W);
     const size_t n = (size_t)pitch * H;
     CK(ctx->a.ensure(n));
     CK(ctx->b.ensure(n));
     CK(ctx->m.ensure(n));
-    if ((st = h2d(ctx->a.p, pitch, in, W, H, ctx->stream))) return st;
-    if ((st = h2d(ctx->b.p, pitch, fallback, W, H, ctx->stream))) return st;
+    if ((st = h2d(ctx->stg, ctx->a.p, pitch, in, W, H, ctx->stream))) return st;
+    if ((st = h2d(ctx->stg, ctx->b.p, pitch, fallback, W, H, ctx->stream))) return st;
     CK(launch_fill_u8(ctx->m.p, 1, n, ctx->stream));
     CK(cudaMemcpy2DAsync(ctx->m.p, pitch, active, W, W, H, cudaMemcpyHostToDevice, ctx->stream));
     Epi e;
     e.mode = EPI_STORE;
     e.active = ctx->m.p;
-    if ((st = run_pass(pl, whole(ctx->a.p, ctx->b.p, pitch, W, H), e, ctx->stream))) return st;
-    if ((st = d2h(out, ctx->b.p, pitch, W, H, ctx->stream))) return st;
+    if ((st = run_pass(ctx, pl, whole(ctx->a.p, ctx->b.p, pitch, W, H), e, ctx->stream))) return st;
+    if ((st = d2h(ctx->stg, out, ctx->b.p, pitch, W, H, ctx->stream))) return st;
     CK(cudaStreamSynchronize(ctx->stream));
     return FDG_OK;
 }
 
+int fdg_conv_apply_masked(fdg_plan* pl, const float* in, int W, int H, const uint8_t* active,
+                          const float* fallback, float* out) {
+    return fdg_conv_apply_masked_ctx(pl ? pl->ctx : nullptr, pl, in, W, H, active, fallback, out);
+}
+}  // extern "C"
+
+namespace {
 // Cache key of a host-buffer RL call: every field of the PSF descriptor, the
-// config and the image size (the solver's plans and graph depend on nothing else).
-static std::string rl_cache_key(const fdg_psf_desc* d, const fdg_rl_config* c, int W, int H) {
+// config, the image size and the engine options (the solver's plans and
+// graph depend on nothing else).
+std::string rl_cache_key(const fdg_psf_desc* d, const fdg_rl_config* c, int W, int H) {
     std::string k;
     auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
-    const int hdr[9] = {d ? d->repr : -1, d ? d->width : 0, d ? d->height : 0, d ? d->anchor_x : 0,
-                        d ? d->anchor_y : 0, d ? d->n_rows : 0, d ? d->n_taps : 0, W, H};
+    const int hdr[10] = {d ? d->repr : -1, d ? d->width : 0, d ? d->height : 0, d ? d->anchor_x : 0,
+                         d ? d->anchor_y : 0, d ? d->n_rows : 0, d ? d->n_taps : 0, W, H, options_key()};
     put(hdr, sizeof hdr);
     put(&c->iterations, sizeof c->iterations);
     put(&c->op, sizeof c->op);
@@ -895,6 +1043,241 @@ static std::string rl_cache_key(const fdg_psf_desc* d, const fdg_rl_config* c, i
     return k;
 }
 
+// ------------------------------------------------------- solver internals
+// (callers hold the context's Entry)
+int solver_create(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, int W, int H, int batch,
+                  std::unique_ptr<fdg_solver>* out) {
+    if (!cfg) return set_err(FDG_EINVAL, "null argument");
+    if (W < 1 || H < 1 || batch < 1) return set_err(FDG_EINVAL, "solver: empty input image");
+    if (!(cfg->epsilon_div > 0.0)) return set_err(FDG_EINVAL, "solver: epsilonDiv must be positive");
+    auto s = std::make_unique<fdg_solver>();
+    s->ctx = ctx;
+    s->cfg = *cfg;
+    s->W = W;
+    s->H = H;
+    s->batch = batch;
+    int st = make_rl_plans(ctx, desc, cfg->op, &s->fwd, &s->adj);
+    if (st) return st;
+    s->ntrace = std::max(cfg->iterations, 1);
+    CK(s->maxchange.ensure(s->ntrace));
+    CK(s->nanflag.ensure(s->ntrace));
+    CK(s->tstamp.ensure(s->ntrace + 1));
+    CK(cudaMemset(s->maxchange.p, 0, sizeof(unsigned) * s->ntrace));
+    CK(cudaMemset(s->nanflag.p, 0, sizeof(int) * s->ntrace));
+    CK(cudaMemset(s->tstamp.p, 0, sizeof(unsigned long long) * (s->ntrace + 1)));
+    *out = std::move(s);
+    return FDG_OK;
+}
+
+int solver_reset_trace(fdg_solver* s) {
+    cudaStream_t st = s->ctx->stream;
+    CK(cudaMemsetAsync(s->maxchange.p, 0, sizeof(unsigned) * s->ntrace, st));
+    CK(cudaMemsetAsync(s->nanflag.p, 0, sizeof(int) * s->ntrace, st));
+    CK(cudaMemsetAsync(s->tstamp.p, 0, sizeof(unsigned long long) * (s->ntrace + 1), st));
+    return FDG_OK;
+}
+
+TraceSlots solver_slots(const fdg_solver* s) { return TraceSlots{s->maxchange.p, s->nanflag.p, s->tstamp.p}; }
+
+int solver_pass(fdg_solver* s, int pass, const float* d_in, const float* d_aux, float* d_out, int pitch,
+                long long image_stride, int y0, int y1, int ylo, int yhi, int iteration) {
+    Geom g;
+    g.in = d_in;
+    g.out = d_out;
+    g.pitch = pitch;
+    g.W = s->W;
+    g.y0 = y0;
+    g.y1 = y1;
+    g.ylo = ylo;
+    g.yhi = yhi;
+    g.batch = s->batch;
+    g.bstride = image_stride;
+    Epi e;
+    if (pass == 1) {
+        e.mode = EPI_QUOT;
+        e.aux = d_aux;
+        e.eps = (float)s->cfg.epsilon_div;
+        return run_pass(s->ctx, s->fwd.get(), g, e, s->ctx->stream);
+    }
+    if (pass == 2) {
+        const int slot = std::min(std::max(iteration, 0), s->ntrace - 1);
+        const TraceSlots tr = solver_slots(s);
+        e.mode = EPI_UPDATE;
+        e.aux = d_aux;
+        e.clamp = s->cfg.clamp_nonnegative;
+        e.maxchange = tr.mc_at(slot);
+        e.nanflag = tr.nf_at(slot);
+        e.tend = tr.end_at(slot);
+        return run_pass(s->ctx, s->adj.get(), g, e, s->ctx->stream);
+    }
+    return set_err(FDG_EINVAL, "pass must be 1 or 2");
+}
+
+int solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long image_stride, int iterations) {
+    if (!d_f || !d_u) return set_err(FDG_EINVAL, "null argument");
+    if (iterations < 0) return set_err(FDG_EINVAL, "solver: iterations must be >= 0");
+    if (pitch % 4 || pitch < s->W) return set_err(FDG_EINVAL, "pitch must be a multiple of 4 and >= width");
+    if (s->batch > 1 && image_stride < (long long)pitch * s->H) return set_err(FDG_EINVAL, "image_stride too small");
+    fdg_ctx* ctx = s->ctx;
+    const long long stride = s->batch > 1 ? image_stride : (long long)pitch * s->H;
+    const size_t n = (size_t)stride * s->batch;
+    CK(s->q.ensure(n));
+    cudaStream_t user = ctx->stream;
+    // Replay the captured graph when the arguments and options are unchanged:
+    // the whole run (start stamp + every iteration's launches) is one
+    // cudaGraphLaunch.
+    static const bool no_graph = getenv("FDG_NO_GRAPH") != nullptr;
+    if (!no_graph && !s->gstream) {
+        CK(cudaStreamCreateWithFlags(&s->gstream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming));
+    }
+    const int opts = options_key();
+    if (!no_graph && s->gexec && s->g_f == d_f && s->g_u == d_u && s->g_pitch == pitch && s->g_stride == stride &&
+        s->g_iters == iterations && s->g_opts == opts) {
+        CK(cudaEventRecord(s->ev_in, user));
+        CK(cudaStreamWaitEvent(s->gstream, s->ev_in, 0));
+        CK(cudaGraphLaunch(s->gexec, s->gstream));
+        CK(cudaEventRecord(s->ev_out, s->gstream));
+        CK(cudaStreamWaitEvent(user, s->ev_out, 0));
+        ctx->launches += s->g_launches;
+        return FDG_OK;
+    }
+    const uint64_t before = ctx->launches;
+    const bool rowres = use_rowres(s->fwd.get(), s->W) && iterations > 0 && iterations <= s->ntrace;
+    const bool fused = !rowres && use_fused(s->fwd.get());
+    const TraceSlots tr = solver_slots(s);
+    auto issue = [&]() -> int {
+        cudaStream_t st = ctx->stream;
+        if (rowres)  // writes its own start stamp
+            return run_rowres(ctx, s->fwd.get(), d_f, d_u, pitch, s->W, s->H, s->batch, stride, iterations, &s->cfg,
+                              tr, st);
+        CK(launch_stamp(tr.ts, st));
+        ctx->launches += 1;
+        if (fused) {
+            for (int k = 0; k < iterations; ++k) {
+                // ping-pong so the result lands in d_u; iteration 0 reads f itself (u0 = f)
+                float* dst = ((iterations - 1 - k) & 1) ? s->q.p : d_u;
+                const float* src = k == 0 ? d_f : (dst == d_u ? s->q.p : d_u);
+                const int slot = std::min(k, s->ntrace - 1);
+                int r = run_fused(ctx, s->fwd.get(), src, d_f, dst, pitch, s->W, s->H, s->batch, stride, &s->cfg,
+                                  tr.mc_at(slot), tr.nf_at(slot), tr.end_at(slot), st);
+                if (r) return r;
+            }
+            if (iterations == 0) CK(cudaMemcpyAsync(d_u, d_f, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+            return FDG_OK;
+        }
+        CK(cudaMemcpyAsync(d_u, d_f, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        for (int k = 0; k < iterations; ++k) {
+            int r = solver_pass(s, 1, d_u, d_f, s->q.p, pitch, stride, 0, s->H, 0, s->H - 1, k);
+            if (r) return r;
+            r = solver_pass(s, 2, s->q.p, d_u, d_u, pitch, stride, 0, s->H, 0, s->H - 1, k);
+            if (r) return r;
+        }
+        return FDG_OK;
+    };
+    if (no_graph) return issue();
+    // first call with these arguments runs eagerly (sets kernel attributes,
+    // surfaces errors with a clear origin), then is captured for replay
+    int r = issue();
+    if (r) return r;
+    if (s->gexec) {
+        cudaGraphExecDestroy(s->gexec);
+        s->gexec = nullptr;
+    }
+    cudaGraph_t graph = nullptr;
+    ctx->stream = s->gstream;  // the passes launch on ctx->stream
+    CK(cudaStreamBeginCapture(s->gstream, cudaStreamCaptureModeThreadLocal));
+    const uint64_t cap0 = ctx->launches;
+    r = issue();
+    cudaError_t ce = cudaStreamEndCapture(s->gstream, &graph);
+    ctx->stream = user;
+    if (r) {
+        if (graph) cudaGraphDestroy(graph);
+        return r;
+    }
+    if (ce != cudaSuccess) return cuda_err(ce, "cudaStreamEndCapture");
+    ce = cudaGraphInstantiate(&s->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) return cuda_err(ce, "cudaGraphInstantiate");
+    s->g_launches = ctx->launches - cap0;
+    ctx->launches = before + s->g_launches;  // the eager run; the capture issued nothing
+    s->g_f = d_f;
+    s->g_u = d_u;
+    s->g_pitch = pitch;
+    s->g_stride = stride;
+    s->g_iters = iterations;
+    s->g_opts = opts;
+    return FDG_OK;
+}
+
+// Per-iteration {max|du|, NaN flag, seconds} of the solver's last run
+// (synchronises).  seconds: differences of the device stamps (0 when an
+// iteration was not stamped, e.g. strip passes).
+int solver_trace(fdg_solver* s, int n, std::vector<float>* mc, std::vector<int>* nf, std::vector<double>* sec) {
+    cudaStream_t st = s->ctx->stream;
+    n = std::min(n, s->ntrace);
+    std::vector<unsigned> m(n);
+    std::vector<unsigned long long> ts(n + 1);
+    nf->assign(n, 0);
+    CK(cudaMemcpyAsync(m.data(), s->maxchange.p, sizeof(unsigned) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(nf->data(), s->nanflag.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ts.data(), s->tstamp.p, sizeof(unsigned long long) * (n + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    mc->resize(n);
+    sec->assign(n, 0.0);
+    for (int k = 0; k < n; ++k) {
+        std::memcpy(&(*mc)[k], &m[k], sizeof(float));
+        if (ts[k] && ts[k + 1] > ts[k]) (*sec)[k] = (double)(ts[k + 1] - ts[k]) * 1e-9;
+    }
+    return FDG_OK;
+}
+
+// rlStepPlanned (rl.hpp:101-125) on host buffers with the caller's plans
+int rl_step_impl(fdg_ctx* ctx, const fdg_plan* fwd, const fdg_plan* adj, const fdg_rl_config* cfg, const float* u,
+                 const float* f, int W, int H, float* u_out, double* max_abs_change) {
+    const int pitch = pitch_for(W);
+    const size_t n = (size_t)pitch * H;
+    cudaStream_t s = ctx->stream;
+    DevBuf<float> df, du, dq;
+    DevBuf<unsigned> mc;
+    DevBuf<int> nf;
+    CK(df.ensure(n));
+    CK(du.ensure(n));
+    CK(dq.ensure(n));
+    CK(mc.ensure(1));
+    CK(nf.ensure(1));
+    CK(cudaMemsetAsync(mc.p, 0, sizeof(unsigned), s));
+    CK(cudaMemsetAsync(nf.p, 0, sizeof(int), s));
+    int st;
+    if ((st = h2d(ctx->stg, df.p, pitch, f, W, H, s))) return st;
+    if ((st = h2d(ctx->stg, du.p, pitch, u, W, H, s))) return st;
+    Epi e1;
+    e1.mode = EPI_QUOT;
+    e1.aux = df.p;
+    e1.eps = (float)cfg->epsilon_div;
+    if ((st = run_pass(ctx, fwd, whole(du.p, dq.p, pitch, W, H), e1, s))) return st;
+    Epi e2;
+    e2.mode = EPI_UPDATE;
+    e2.aux = du.p;
+    e2.clamp = cfg->clamp_nonnegative;
+    e2.maxchange = mc.p;
+    e2.nanflag = nf.p;
+    if ((st = run_pass(ctx, adj, whole(dq.p, du.p, pitch, W, H), e2, s))) return st;
+    if ((st = d2h(ctx->stg, u_out, du.p, pitch, W, H, s))) return st;
+    unsigned m = 0;
+    CK(cudaMemcpyAsync(&m, mc.p, sizeof m, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (max_abs_change) {
+        float fm;
+        std::memcpy(&fm, &m, sizeof fm);
+        *max_abs_change = fm;
+    }
+    return FDG_OK;
+}
+}  // namespace
+
+extern "C" {
 int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, const float* f, int W,
                       int H, float* u_out, fdg_rl_record* trace) {
     PhaseTimer pt;
@@ -902,11 +1285,13 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     if (st) return st;
     if (!ctx) {  // no device: validate on the host so the reference's errors still surface
         if ((st = validate_rl(f, W, H, cfg, "rlDeconvolve"))) return st;
-        return check_device(ctx);
+        Entry en;
+        return enter(ctx, en);
     }
-    if ((st = check_device(ctx))) return st;
-    // Repeated calls with the same PSF / config / size replay the solver's
-    // captured graph (one cudaGraphLaunch for the whole iteration loop)
+    Entry en;
+    if ((st = enter(ctx, en))) return st;
+    // Repeated calls with the same PSF / config / size / options replay the
+    // solver's captured graph (one cudaGraphLaunch for the whole loop)
     static const bool no_cache = getenv("FDG_NO_RL_CACHE") != nullptr;
     fdg_solver* sv = nullptr;
     if (!no_cache && cfg->iterations >= 1) {
@@ -915,9 +1300,9 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
             fdg_solver_destroy(ctx->rl_solver);
             ctx->rl_solver = nullptr;
             ctx->rl_key.clear();
-            fdg_solver* ns = nullptr;
-            if ((st = fdg_solver_create(ctx, desc, cfg, W, H, 1, &ns))) return st;
-            ctx->rl_solver = ns;
+            std::unique_ptr<fdg_solver> ns;
+            if ((st = solver_create(ctx, desc, cfg, W, H, 1, &ns))) return st;
+            ctx->rl_solver = ns.release();
             ctx->rl_key = std::move(key);
         }
         sv = ctx->rl_solver;
@@ -934,54 +1319,45 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     CK(ctx->c.ensure(n));  // q
     CK(ctx->tr_max.ensure(iters + 1));
     CK(ctx->tr_nan.ensure(iters + 1));
+    CK(ctx->tr_time.ensure(iters + 2));
     float *df = ctx->a.p, *du = ctx->b.p, *dq = ctx->c.p;
-    unsigned* mc = ctx->tr_max.p;
-    int* nf = ctx->tr_nan.p;
     pt.mark("alloc");
-    if ((st = h2d(df, pitch, f, W, H, s))) return st;
+    if ((st = h2d(ctx->stg, df, pitch, f, W, H, s))) return st;
     if ((st = validate_device(ctx, df, W, H, pitch, "rlDeconvolve"))) return st;
     pt.mark("h2d+validate");
     if (sv) {
-        EventPool ev;
-        if (trace) {
-            CK(ev.make(2));
-            CK(cudaEventRecord(ev.ev[0], s));
-        }
-        if ((st = fdg_solver_reset_trace(sv))) return st;
-        if ((st = fdg_solver_run(sv, df, du, pitch, 0, iters))) return st;
-        if (trace) CK(cudaEventRecord(ev.ev[1], s));
+        if ((st = solver_reset_trace(sv))) return st;
+        if ((st = solver_run(sv, df, du, pitch, 0, iters))) return st;
         prefault(u_out, (size_t)W * H * sizeof(float));
         if (pt.on) {
             CK(cudaStreamSynchronize(s));
             pt.mark("iterate(graph)");
         }
-        if ((st = d2h(u_out, du, pitch, W, H, s))) return st;
-        std::vector<fdg_rl_record> rec(iters);
-        if ((st = fdg_solver_trace(sv, rec.data(), iters))) return st;  // synchronises the stream
+        if ((st = d2h(ctx->stg, u_out, du, pitch, W, H, s))) return st;
+        std::vector<float> mc;
+        std::vector<int> nf;
+        std::vector<double> sec;
+        if ((st = solver_trace(sv, iters, &mc, &nf, &sec))) return st;  // synchronises the stream
         pt.mark("d2h");
-        float ms = 0.f;
-        if (trace) cudaEventElapsedTime(&ms, ev.ev[0], ev.ev[1]);
         for (int k = 0; k < iters; ++k) {
-            if (rec[k].inactive_fraction != 0.0)  // the solver trace's NaN slot
-                return set_err(FDG_ENAN, "rlDeconvolve: NaN in iterate at iteration " + std::to_string(k + 1));
-            // one graph for the whole loop: per-iteration seconds = run time / iterations
-            if (trace) trace[k] = {k + 1, 0.0, rec[k].max_abs_change, ms * 1e-3 / iters};
+            if (nf[k]) return set_err(FDG_ENAN, "rlDeconvolve: NaN in iterate at iteration " + std::to_string(k + 1));
+            // per-iteration seconds from the device stamps of the replayed graph
+            if (trace) trace[k] = {k + 1, 0.0, (double)mc[k], sec[k]};
         }
         return FDG_OK;
     }
-    CK(cudaMemsetAsync(mc, 0, sizeof(unsigned) * (iters + 1), s));
-    CK(cudaMemsetAsync(nf, 0, sizeof(int) * (iters + 1), s));
+    // uncached (FDG_NO_RL_CACHE, or 0 iterations): launch the loop directly
+    const TraceSlots tr{ctx->tr_max.p, ctx->tr_nan.p, ctx->tr_time.p};
+    CK(cudaMemsetAsync(tr.mc, 0, sizeof(unsigned) * (iters + 1), s));
+    CK(cudaMemsetAsync(tr.nf, 0, sizeof(int) * (iters + 1), s));
+    CK(cudaMemsetAsync(tr.ts, 0, sizeof(unsigned long long) * (iters + 2), s));
     CK(cudaMemcpyAsync(du, df, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
-    EventPool ev;
-    const bool timed = trace != nullptr;
     const bool rowres = use_rowres(fwd.get(), W) && iters > 0;
-    if (timed) {
-        CK(ev.make(iters + 1));
-        CK(cudaEventRecord(ev.ev[0], s));
-    }
-    if (rowres) {  // all iterations in one launch; per-iteration seconds = run time / iterations
-        if ((st = run_rowres(fwd.get(), df, du, pitch, W, H, 1, 0, iters, cfg, mc, nf, s))) return st;
-        if (timed) CK(cudaEventRecord(ev.ev[iters], s));
+    if (rowres) {
+        if ((st = run_rowres(ctx, fwd.get(), df, du, pitch, W, H, 1, 0, iters, cfg, tr, s))) return st;
+    } else {
+        CK(launch_stamp(tr.ts, s));
+        ctx->launches += 1;
     }
     const bool fused = !rowres && use_fused(fwd.get());
     for (int k = 0; fused && k < iters; ++k) {
@@ -989,23 +1365,24 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
         // (iters - 1 - k) is even; iteration 0 reads f itself (u0 = f)
         float* dst = ((iters - 1 - k) & 1) ? dq : du;
         const float* src = k == 0 ? df : (dst == du ? dq : du);
-        if ((st = run_fused(fwd.get(), src, df, dst, pitch, W, H, 1, 0, cfg, mc + k, nf + k, s))) return st;
-        if (timed) CK(cudaEventRecord(ev.ev[k + 1], s));
+        if ((st = run_fused(ctx, fwd.get(), src, df, dst, pitch, W, H, 1, 0, cfg, tr.mc_at(k), tr.nf_at(k),
+                            tr.end_at(k), s)))
+            return st;
     }
     for (int k = 0; k < (rowres || fused ? 0 : iters); ++k) {
         Epi e1;
         e1.mode = EPI_QUOT;
         e1.aux = df;
         e1.eps = (float)cfg->epsilon_div;
-        if ((st = run_pass(fwd.get(), whole(du, dq, pitch, W, H), e1, s))) return st;
+        if ((st = run_pass(ctx, fwd.get(), whole(du, dq, pitch, W, H), e1, s))) return st;
         Epi e2;
         e2.mode = EPI_UPDATE;
         e2.aux = du;
         e2.clamp = cfg->clamp_nonnegative;
-        e2.maxchange = mc + k;
-        e2.nanflag = nf + k;
-        if ((st = run_pass(adj.get(), whole(dq, du, pitch, W, H), e2, s))) return st;
-        if (timed) CK(cudaEventRecord(ev.ev[k + 1], s));
+        e2.maxchange = tr.mc_at(k);
+        e2.nanflag = tr.nf_at(k);
+        e2.tend = tr.end_at(k);
+        if ((st = run_pass(ctx, adj.get(), whole(dq, du, pitch, W, H), e2, s))) return st;
     }
     // While the device iterates, fault in the (pageable) output pages on the
     // host so the final D2H does not pay first-touch page faults.
@@ -1014,25 +1391,22 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
         CK(cudaStreamSynchronize(s));
         pt.mark("iterate");
     }
-    if ((st = d2h(u_out, du, pitch, W, H, s))) return st;
+    if ((st = d2h(ctx->stg, u_out, du, pitch, W, H, s))) return st;
     std::vector<unsigned> hmc(iters + 1);
     std::vector<int> hnf(iters + 1);
-    CK(cudaMemcpyAsync(hmc.data(), mc, sizeof(unsigned) * (iters + 1), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hnf.data(), nf, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost, s));
+    std::vector<unsigned long long> hts(iters + 2);
+    CK(cudaMemcpyAsync(hmc.data(), tr.mc, sizeof(unsigned) * (iters + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hnf.data(), tr.nf, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hts.data(), tr.ts, sizeof(unsigned long long) * (iters + 2), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     pt.mark("d2h");
     for (int k = 0; k < iters; ++k) {
-        if (hnf[k])
-            return set_err(FDG_ENAN, "rlDeconvolve: NaN in iterate at iteration " + std::to_string(k + 1));
+        if (hnf[k]) return set_err(FDG_ENAN, "rlDeconvolve: NaN in iterate at iteration " + std::to_string(k + 1));
         if (trace) {
-            float ms = 0.f;
-            if (rowres)
-                cudaEventElapsedTime(&ms, ev.ev[0], ev.ev[iters]), ms /= (float)iters;
-            else
-                cudaEventElapsedTime(&ms, ev.ev[k], ev.ev[k + 1]);
             float m;
             std::memcpy(&m, &hmc[k], sizeof m);
-            trace[k] = {k + 1, 0.0, (double)m, ms * 1e-3};
+            const double sec = hts[k] && hts[k + 1] > hts[k] ? (double)(hts[k + 1] - hts[k]) * 1e-9 : 0.0;
+            trace[k] = {k + 1, 0.0, (double)m, sec};
         }
     }
     return FDG_OK;
@@ -1042,47 +1416,23 @@ int fdg_rl_step(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg
                 int W, int H, float* u_out, double* max_abs_change) {
     if (!u || !f || !u_out || !cfg) return set_err(FDG_EINVAL, "null argument");
     if (W < 1 || H < 1) return set_err(FDG_EINVAL, "rlStep: image dimensions differ");
-    int st = check_device(ctx);
+    Entry en;
+    int st = enter(ctx, en);
     if (st) return st;
     std::unique_ptr<fdg_plan> fwd, adj;
     if ((st = make_rl_plans(ctx, desc, cfg->op, &fwd, &adj))) return st;
-    const int pitch = pitch_for(W);
-    const size_t n = (size_t)pitch * H;
-    cudaStream_t s = ctx->stream;
-    DevBuf<float> df, du, dq;
-    DevBuf<unsigned> mc;
-    DevBuf<int> nf;
-    CK(df.ensure(n));
-    CK(du.ensure(n));
-    CK(dq.ensure(n));
-    CK(mc.ensure(1));
-    CK(nf.ensure(1));
-    CK(cudaMemsetAsync(mc.p, 0, sizeof(unsigned), s));
-    CK(cudaMemsetAsync(nf.p, 0, sizeof(int), s));
-    if ((st = h2d(df.p, pitch, f, W, H, s))) return st;
-    if ((st = h2d(du.p, pitch, u, W, H, s))) return st;
-    Epi e1;
-    e1.mode = EPI_QUOT;
-    e1.aux = df.p;
-    e1.eps = (float)cfg->epsilon_div;
-    if ((st = run_pass(fwd.get(), whole(du.p, dq.p, pitch, W, H), e1, s))) return st;
-    Epi e2;
-    e2.mode = EPI_UPDATE;
-    e2.aux = du.p;
-    e2.clamp = cfg->clamp_nonnegative;
-    e2.maxchange = mc.p;
-    e2.nanflag = nf.p;
-    if ((st = run_pass(adj.get(), whole(dq.p, du.p, pitch, W, H), e2, s))) return st;
-    if ((st = d2h(u_out, du.p, pitch, W, H, s))) return st;
-    unsigned m = 0;
-    CK(cudaMemcpyAsync(&m, mc.p, sizeof m, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (max_abs_change) {
-        float fm;
-        std::memcpy(&fm, &m, sizeof fm);
-        *max_abs_change = fm;
-    }
-    return FDG_OK;
+    return rl_step_impl(ctx, fwd.get(), adj.get(), cfg, u, f, W, H, u_out, max_abs_change);
+}
+
+int fdg_rl_step_planned(fdg_ctx* ctx, const fdg_plan* forward, const fdg_plan* adjoint, const fdg_rl_config* cfg,
+                        const float* u, const float* f, int W, int H, float* u_out, double* max_abs_change) {
+    if (!forward || !adjoint || !u || !f || !u_out || !cfg) return set_err(FDG_EINVAL, "null argument");
+    if (W < 1 || H < 1) return set_err(FDG_EINVAL, "rlStep: image dimensions differ");
+    Entry en;
+    int st = enter(ctx, en);
+    if (st) return st;
+    if ((st = check_plan_ctx(ctx, forward)) || (st = check_plan_ctx(ctx, adjoint))) return st;
+    return rl_step_impl(ctx, forward, adjoint, cfg, u, f, W, H, u_out, max_abs_change);
 }
 
 int fdg_rl_deconvolve_selective(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, double threshold,
@@ -1097,7 +1447,8 @@ int fdg_rl_deconvolve_selective(fdg_ctx* ctx, const fdg_psf_desc* desc, const fd
     if (kind == FDG_OP_AUTO) kind = desc && desc->repr == FDG_PSF_SPARSE ? FDG_OP_LIST : FDG_OP_NAIVE;
     if (kind != FDG_OP_NAIVE && kind != FDG_OP_LIST)
         return set_err(FDG_EINVAL, "operator does not support masked evaluation");
-    if ((st = check_device(ctx))) return st;
+    Entry en;
+    if ((st = enter(ctx, en))) return st;
     std::unique_ptr<fdg_plan> fwd, adj;
     if ((st = make_rl_plans(ctx, desc, kind, &fwd, &adj))) return st;
     const int iters = cfg->iterations;
@@ -1122,7 +1473,7 @@ int fdg_rl_deconvolve_selective(fdg_ctx* ctx, const fdg_psf_desc* desc, const fd
     CK(cudaMemsetAsync(ni.p, 0, sizeof(unsigned long long) * (iters + 1), s));
     CK(cudaMemsetAsync(dv.p, 0, n * sizeof(float), s));  // cachedV = 0 (rl.hpp:212)
     CK(launch_fill_u8(dm.p, 1, n, s));                     // all active; pitch padding stays 1
-    if ((st = h2d(df.p, pitch, f, W, H, s))) return st;
+    if ((st = h2d(ctx->stg, df.p, pitch, f, W, H, s))) return st;
     CK(cudaMemcpyAsync(du.p, df.p, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
     CK(launch_quot_const(df.p, dq.p, W, H, pitch, 0, 1, 0.f, (float)cfg->epsilon_div, s));
     EventPool ev;
@@ -1153,12 +1504,12 @@ int fdg_rl_deconvolve_selective(fdg_ctx* ctx, const fdg_psf_desc* desc, const fd
             // compaction (also counts inactive pixels) then the thinned dense pass
             const DenseTiling t = dense_tiling(W, H);
             const size_t tiles = (size_t)t.tiles_x * t.tiles_y;
-            CK(fwd->tile_blocks.ensure(tiles * 256));
-            CK(fwd->tile_count.ensure(tiles));
-            CK(launch_tile_compact(dm.p, W, H, pitch, fwd->tile_blocks.p, fwd->tile_count.p, ni.p + k, s));
-            CK(launch_dense(fwd->dev, whole(du.p, dq.p, pitch, W, H), e1, s, fwd->tile_blocks.p, fwd->tile_count.p));
+            CK(ctx->tile_blocks.ensure(tiles * 256));
+            CK(ctx->tile_count.ensure(tiles));
+            CK(launch_tile_compact(dm.p, W, H, pitch, ctx->tile_blocks.p, ctx->tile_count.p, ni.p + k, s));
+            CK(launch_dense(fwd->dev, whole(du.p, dq.p, pitch, W, H), e1, s, ctx->tile_blocks.p, ctx->tile_count.p));
             ctx->launches += 2;
-        } else if ((st = run_pass(fwd.get(), whole(du.p, dq.p, pitch, W, H), e1, s))) {
+        } else if ((st = run_pass(ctx, fwd.get(), whole(du.p, dq.p, pitch, W, H), e1, s))) {
             return st;
         }
         Epi e2;
@@ -1172,14 +1523,14 @@ int fdg_rl_deconvolve_selective(fdg_ctx* ctx, const fdg_psf_desc* desc, const fd
         e2.may_thin = (!mask_replay && k >= thin_start) ? 1 : 0;
         if (dense) {
             // the adjoint pass sees the same mask: reuse the forward's lists
-            CK(launch_dense(adj->dev, whole(dq.p, du.p, pitch, W, H), e2, s, fwd->tile_blocks.p, fwd->tile_count.p));
+            CK(launch_dense(adj->dev, whole(dq.p, du.p, pitch, W, H), e2, s, ctx->tile_blocks.p, ctx->tile_count.p));
             ctx->launches += 1;
-        } else if ((st = run_pass(adj.get(), whole(dq.p, du.p, pitch, W, H), e2, s))) {
+        } else if ((st = run_pass(ctx, adj.get(), whole(dq.p, du.p, pitch, W, H), e2, s))) {
             return st;
         }
         CK(cudaEventRecord(ev.ev[k + 1], s));
     }
-    if ((st = d2h(u_out, du.p, pitch, W, H, s))) return st;
+    if ((st = d2h(ctx->stg, u_out, du.p, pitch, W, H, s))) return st;
     std::vector<unsigned> hmc(iters + 1);
     std::vector<int> hnf(iters + 1);
     std::vector<unsigned long long> hni(iters + 1);
@@ -1206,22 +1557,13 @@ int fdg_rl_deconvolve_selective(fdg_ctx* ctx, const fdg_psf_desc* desc, const fd
 int fdg_solver_create(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, int W, int H, int batch,
                       fdg_solver** out) {
     if (!cfg || !out) return set_err(FDG_EINVAL, "null argument");
-    if (W < 1 || H < 1 || batch < 1) return set_err(FDG_EINVAL, "solver: empty input image");
-    if (!(cfg->epsilon_div > 0.0)) return set_err(FDG_EINVAL, "solver: epsilonDiv must be positive");
-    int st = check_device(ctx);
+    Entry en;
+    int st = enter(ctx, en);
     if (st) return st;
-    auto s = std::make_unique<fdg_solver>();
-    s->ctx = ctx;
-    s->cfg = *cfg;
-    s->W = W;
-    s->H = H;
-    s->batch = batch;
-    if ((st = make_rl_plans(ctx, desc, cfg->op, &s->fwd, &s->adj))) return st;
-    s->ntrace = std::max(cfg->iterations, 1);
-    CK(s->maxchange.ensure(s->ntrace));
-    CK(s->nanflag.ensure(s->ntrace));
-    CK(cudaMemset(s->maxchange.p, 0, sizeof(unsigned) * s->ntrace));
-    CK(cudaMemset(s->nanflag.p, 0, sizeof(int) * s->ntrace));
+    std::unique_ptr<fdg_solver> s;
+    if ((st = solver_create(ctx, desc, cfg, W, H, batch, &s))) return st;
+    ctx_retain(ctx);
+    s->holds_ref = true;
     *out = s.release();
     return FDG_OK;
 }
@@ -1230,9 +1572,10 @@ void fdg_solver_destroy(fdg_solver* s) { delete s; }
 
 int fdg_solver_reset_trace(fdg_solver* s) {
     if (!s) return set_err(FDG_EINVAL, "null solver");
-    CK(cudaMemsetAsync(s->maxchange.p, 0, sizeof(unsigned) * s->ntrace, s->ctx->stream));
-    CK(cudaMemsetAsync(s->nanflag.p, 0, sizeof(int) * s->ntrace, s->ctx->stream));
-    return FDG_OK;
+    Entry en;
+    int st = enter(s->ctx, en);
+    if (st) return st;
+    return solver_reset_trace(s);
 }
 
 int fdg_solver_pass(fdg_solver* s, int pass, const float* d_in, const float* d_aux, float* d_out, int pitch,
@@ -1240,34 +1583,10 @@ int fdg_solver_pass(fdg_solver* s, int pass, const float* d_in, const float* d_a
     if (!s || !d_in || !d_aux || !d_out) return set_err(FDG_EINVAL, "null argument");
     if (pitch % 4 || pitch < s->W) return set_err(FDG_EINVAL, "pitch must be a multiple of 4 and >= width");
     if (ylo > yhi || y0 > y1) return set_err(FDG_EINVAL, "empty row range");
-    Geom g;
-    g.in = d_in;
-    g.out = d_out;
-    g.pitch = pitch;
-    g.W = s->W;
-    g.y0 = y0;
-    g.y1 = y1;
-    g.ylo = ylo;
-    g.yhi = yhi;
-    g.batch = s->batch;
-    g.bstride = image_stride;
-    Epi e;
-    if (pass == 1) {
-        e.mode = EPI_QUOT;
-        e.aux = d_aux;
-        e.eps = (float)s->cfg.epsilon_div;
-        return run_pass(s->fwd.get(), g, e, s->ctx->stream);
-    }
-    if (pass == 2) {
-        const int slot = std::min(std::max(iteration, 0), s->ntrace - 1);
-        e.mode = EPI_UPDATE;
-        e.aux = d_aux;
-        e.clamp = s->cfg.clamp_nonnegative;
-        e.maxchange = s->maxchange.p + slot;
-        e.nanflag = s->nanflag.p + slot;
-        return run_pass(s->adj.get(), g, e, s->ctx->stream);
-    }
-    return set_err(FDG_EINVAL, "pass must be 1 or 2");
+    Entry en;
+    int st = enter(s->ctx, en);
+    if (st) return st;
+    return solver_pass(s, pass, d_in, d_aux, d_out, pitch, image_stride, y0, y1, ylo, yhi, iteration);
 }
 
 int fdg_solver_iterate(fdg_solver* s, const float* d_f, const float* d_u_in, float* d_u_out, int pitch,
@@ -1277,102 +1596,22 @@ int fdg_solver_iterate(fdg_solver* s, const float* d_f, const float* d_u_in, flo
     if (!use_fused(s->fwd.get())) return set_err(FDG_EINVAL, "solver engine is not fused (see fdg_solver_engine)");
     if (pitch % 4 || pitch < s->W) return set_err(FDG_EINVAL, "pitch must be a multiple of 4 and >= width");
     if (ylo > yhi || y0 > y1 || y0 < ylo || y1 - 1 > yhi) return set_err(FDG_EINVAL, "bad row ranges");
+    Entry en;
+    int st = enter(s->ctx, en);
+    if (st) return st;
     const int slot = std::min(std::max(iteration, 0), s->ntrace - 1);
     const long long stride = s->batch > 1 ? image_stride : 0;
-    return run_fused(s->fwd.get(), d_u_in, d_f, d_u_out, pitch, s->W, s->H, s->batch, stride, &s->cfg,
-                     s->maxchange.p + slot, s->nanflag.p + slot, s->ctx->stream, y0, y1, ylo, yhi);
+    const TraceSlots tr = solver_slots(s);
+    return run_fused(s->ctx, s->fwd.get(), d_u_in, d_f, d_u_out, pitch, s->W, s->H, s->batch, stride, &s->cfg,
+                     tr.mc_at(slot), tr.nf_at(slot), tr.end_at(slot), s->ctx->stream, y0, y1, ylo, yhi);
 }
 
 int fdg_solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long image_stride, int iterations) {
-    if (!s || !d_f || !d_u) return set_err(FDG_EINVAL, "null argument");
-    if (iterations < 0) return set_err(FDG_EINVAL, "solver: iterations must be >= 0");
-    if (pitch % 4 || pitch < s->W) return set_err(FDG_EINVAL, "pitch must be a multiple of 4 and >= width");
-    if (s->batch > 1 && image_stride < (long long)pitch * s->H) return set_err(FDG_EINVAL, "image_stride too small");
-    const long long stride = s->batch > 1 ? image_stride : (long long)pitch * s->H;
-    const size_t n = (size_t)stride * s->batch;
-    CK(s->q.ensure(n));
-    cudaStream_t user = s->ctx->stream;
-    cudaStream_t st = user;
-    // Replay the captured graph when the arguments are unchanged: the whole
-    // run (copy + 2 x iterations fused passes) is one cudaGraphLaunch.
-    static const bool no_graph = getenv("FDG_NO_GRAPH") != nullptr;
-    if (!no_graph && !s->gstream) {
-        CK(cudaStreamCreateWithFlags(&s->gstream, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming));
-    }
-    if (!no_graph && s->gexec && s->g_f == d_f && s->g_u == d_u && s->g_pitch == pitch && s->g_stride == stride &&
-        s->g_iters == iterations) {
-        CK(cudaEventRecord(s->ev_in, user));
-        CK(cudaStreamWaitEvent(s->gstream, s->ev_in, 0));
-        CK(cudaGraphLaunch(s->gexec, s->gstream));
-        CK(cudaEventRecord(s->ev_out, s->gstream));
-        CK(cudaStreamWaitEvent(user, s->ev_out, 0));
-        s->ctx->launches += s->g_launches;
-        return FDG_OK;
-    }
-    const uint64_t before = s->ctx->launches;
-    const bool rowres = use_rowres(s->fwd.get(), s->W) && iterations > 0 && iterations <= s->ntrace;
-    const bool fused = !rowres && use_fused(s->fwd.get());
-    auto issue = [&]() -> int {
-        if (rowres)
-            return run_rowres(s->fwd.get(), d_f, d_u, pitch, s->W, s->H, s->batch, stride, iterations, &s->cfg,
-                              s->maxchange.p, s->nanflag.p, s->ctx->stream);
-        if (fused) {
-            for (int k = 0; k < iterations; ++k) {
-                float* dst = ((iterations - 1 - k) & 1) ? s->q.p : d_u;
-                const float* src = k == 0 ? d_f : (dst == d_u ? s->q.p : d_u);
-                const int slot = std::min(k, s->ntrace - 1);
-                int r = run_fused(s->fwd.get(), src, d_f, dst, pitch, s->W, s->H, s->batch, stride, &s->cfg,
-                                  s->maxchange.p + slot, s->nanflag.p + slot, s->ctx->stream);
-                if (r) return r;
-            }
-            if (iterations == 0)
-                CK(cudaMemcpyAsync(d_u, d_f, n * sizeof(float), cudaMemcpyDeviceToDevice, s->ctx->stream));
-            return FDG_OK;
-        }
-        CK(cudaMemcpyAsync(d_u, d_f, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
-        for (int k = 0; k < iterations; ++k) {
-            int r = fdg_solver_pass(s, 1, d_u, d_f, s->q.p, pitch, stride, 0, s->H, 0, s->H - 1, k);
-            if (r) return r;
-            r = fdg_solver_pass(s, 2, s->q.p, d_u, d_u, pitch, stride, 0, s->H, 0, s->H - 1, k);
-            if (r) return r;
-        }
-        return FDG_OK;
-    };
-    if (no_graph) return issue();
-    // first call with these arguments runs eagerly (sets kernel attributes,
-    // surfaces errors with a clear origin), then is captured for replay
-    int r = issue();
-    if (r) return r;
-    if (s->gexec) {
-        cudaGraphExecDestroy(s->gexec);
-        s->gexec = nullptr;
-    }
-    cudaGraph_t graph = nullptr;
-    st = s->gstream;
-    s->ctx->stream = st;  // the passes launch on ctx->stream
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    const uint64_t cap0 = s->ctx->launches;
-    r = issue();
-    cudaError_t ce = cudaStreamEndCapture(st, &graph);
-    s->ctx->stream = user;
-    if (r) {
-        if (graph) cudaGraphDestroy(graph);
-        return r;
-    }
-    if (ce != cudaSuccess) return cuda_err(ce, "cudaStreamEndCapture");
-    ce = cudaGraphInstantiate(&s->gexec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (ce != cudaSuccess) return cuda_err(ce, "cudaGraphInstantiate");
-    s->g_launches = s->ctx->launches - cap0;
-    s->ctx->launches = before + s->g_launches;  // the eager run; the capture issued nothing
-    s->g_f = d_f;
-    s->g_u = d_u;
-    s->g_pitch = pitch;
-    s->g_stride = stride;
-    s->g_iters = iterations;
-    return FDG_OK;
+    if (!s) return set_err(FDG_EINVAL, "null solver");
+    Entry en;
+    int st = enter(s->ctx, en);
+    if (st) return st;
+    return solver_run(s, d_f, d_u, pitch, image_stride, iterations);
 }
 
 const char* fdg_solver_engine(const fdg_solver* s) {
@@ -1384,24 +1623,23 @@ const char* fdg_solver_engine(const fdg_solver* s) {
 
 int fdg_solver_trace(fdg_solver* s, fdg_rl_record* out, int n) {
     if (!s || !out) return set_err(FDG_EINVAL, "null argument");
-    n = std::min(n, s->ntrace);
-    std::vector<unsigned> mc(n);
-    std::vector<int> nf(n);
-    CK(cudaMemcpyAsync(mc.data(), s->maxchange.p, sizeof(unsigned) * n, cudaMemcpyDeviceToHost, s->ctx->stream));
-    CK(cudaMemcpyAsync(nf.data(), s->nanflag.p, sizeof(int) * n, cudaMemcpyDeviceToHost, s->ctx->stream));
-    CK(cudaStreamSynchronize(s->ctx->stream));
-    for (int k = 0; k < n; ++k) {
-        float m;
-        std::memcpy(&m, &mc[k], sizeof m);
-        out[k] = {k + 1, nf[k] ? 1.0 : 0.0, (double)m, 0.0};  // inactive_fraction slot carries the NaN flag
-    }
+    Entry en;
+    int st = enter(s->ctx, en);
+    if (st) return st;
+    std::vector<float> mc;
+    std::vector<int> nf;
+    std::vector<double> sec;
+    if ((st = solver_trace(s, n, &mc, &nf, &sec))) return st;
+    for (size_t k = 0; k < mc.size(); ++k)  // inactive_fraction slot carries the NaN flag
+        out[k] = {(int)k + 1, nf[k] ? 1.0 : 0.0, (double)mc[k], sec[k]};
     return FDG_OK;
 }
 
 int fdg_mask_compact(fdg_ctx* ctx, const uint8_t* active, int W, int H, int64_t* idx, int64_t idx_cap,
                      int64_t* n_active, int32_t* runs, int64_t runs_cap, int64_t* n_runs) {
     if (!active || W < 1 || H < 1) return set_err(FDG_EINVAL, "empty mask");
-    int st = check_device(ctx);
+    Entry en;
+    int st = enter(ctx, en);
     if (st) return st;
     cudaStream_t s = ctx->stream;
     const size_t n = (size_t)W * H;

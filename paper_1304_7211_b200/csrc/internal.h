@@ -83,6 +83,7 @@ struct Epi {
     int clamp = 1;
     unsigned* maxchange = nullptr;  // float bits, atomicMax
     int* nanflag = nullptr;
+    unsigned long long* tend = nullptr;  // %globaltimer at the end of the pass (atomicMax)
     uint8_t* active = nullptr;      // masked modes / masked store
     float thr = 0.f;
     int may_thin = 0;
@@ -131,7 +132,7 @@ bool rect_supported(int mx);
 bool rowres_supported(int mx, int my, int min_dx, int min_dy, int W);
 cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float* u, int pitch, int W, int H,
                           int batch, long long bstride, int iters, float eps, int clamp, unsigned* maxchange,
-                          int* nanflag, cudaStream_t st);
+                          int* nanflag, unsigned long long* tend, unsigned long long* tbegin, cudaStream_t st);
 // Whole RL iteration in one pass for the centred 15x15 box (kernels_fused.cu):
 // u_out = max(box*(f / max(box(u_in), eps)) * u_in, 0); u_in != u_out.
 bool fused_supported(int mx, int my, int min_dx, int min_dy);
@@ -141,9 +142,11 @@ int fused_mode();
 // between a shard's core and those edges must hold valid halo rows).
 cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int y0, int y1, int ylo,
                          int yhi, int batch, long long bstride, float scale, float eps, int clamp,
-                         unsigned* maxchange, int* nanflag, cudaStream_t st);
+                         unsigned* maxchange, int* nanflag, unsigned long long* tend, cudaStream_t st);
 // first non-finite / first negative row-major index (~0 if none) -> out[0..1]
 cudaError_t launch_validate(const float* f, int W, int H, int pitch, unsigned long long* out, cudaStream_t st);
+// one thread writes %globaltimer to *t (start stamp of a timed RL loop)
+cudaError_t launch_stamp(unsigned long long* t, cudaStream_t st);
 cudaError_t launch_count_inactive(const uint8_t* active, size_t n, unsigned long long* out,
                                   cudaStream_t st);
 

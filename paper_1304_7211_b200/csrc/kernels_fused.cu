@@ -74,6 +74,7 @@ struct FusedArgs {
     int clamp;
     unsigned* maxchange;
     int* nanflag;
+    unsigned long long* tend;
 };
 
 // ---- packed fp32x2 arithmetic (Blackwell FADD2 / FMUL2 / FFMA2)
@@ -497,6 +498,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
             if (lane == 0) {
                 if (bits) atomicMax(a.maxchange, bits);
                 if (anynan) atomicOr(a.nanflag, 1);
+                stamp_end(a.tend);
             }
         }
     };
@@ -587,20 +589,20 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
 
 // Engine selection: 1 = on (default; beats the two-pass engine on config 4),
 // 0 = off; FDG_FUSED=0/1 or fdg_set_option("fused", v).
-int g_fused = getenv("FDG_FUSED") ? atoi(getenv("FDG_FUSED")) : 1;
+std::atomic<int> g_fused{getenv("FDG_FUSED") ? atoi(getenv("FDG_FUSED")) : 1};
 
 }  // namespace
 
-void set_fused_mode(int v) { g_fused = v; }
-int fused_mode() { return g_fused; }
+void set_fused_mode(int v) { g_fused.store(v); }
+int fused_mode() { return g_fused.load(); }
 
 bool fused_supported(int mx, int my, int min_dx, int min_dy) {
-    return g_fused == 1 && mx == 15 && my == 15 && min_dx == -7 && min_dy == -7;
+    return g_fused.load() == 1 && mx == 15 && my == 15 && min_dx == -7 && min_dy == -7;
 }
 
 cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int y0, int y1, int ylo,
                          int yhi, int batch, long long bstride, float scale, float eps, int clamp, unsigned* maxchange, int* nanflag,
-                         cudaStream_t st) {
+                         unsigned long long* tend, cudaStream_t st) {
     FusedArgs a;
     a.u_in = u_in;
     a.f = f;
@@ -619,6 +621,7 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
     a.clamp = clamp;
     a.maxchange = maxchange;
     a.nanflag = nanflag;
+    a.tend = tend;
     static const int variant = getenv("FDG_FUSED_V") ? atoi(getenv("FDG_FUSED_V")) : 0;
     switch (variant) {
         case 1: return launch_t<7, 7, 128, 2, 8, 16>(a, st);

@@ -114,7 +114,14 @@ __global__ void k_row_emit(const uint8_t* act, int W, int H, const long long* ru
     }
 }
 
+__global__ void k_stamp(unsigned long long* t) { *t = globaltimer(); }
+
 }  // namespace
+
+cudaError_t launch_stamp(unsigned long long* t, cudaStream_t st) {
+    k_stamp<<<1, 1, 0, st>>>(t);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_tile_compact(const uint8_t* active, int W, int H, int pitch_mask, int* d_tile_blocks,
                                 int* d_tile_count, unsigned long long* d_inactive, cudaStream_t st) {

@@ -36,6 +36,8 @@ struct RowResArgs {
     int clamp;
     unsigned* maxchange;  // [iters] float bits
     int* nanflag;         // [iters]
+    unsigned long long* tend;  // [iters] %globaltimer at the end of iteration k (max over CTAs)
+    unsigned long long* tbegin;  // start stamp of the run (block 0)
 };
 
 template <int N>
@@ -110,6 +112,7 @@ __global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
     float* sq = sf + R * wp;        // R x wp
     float* smax = sq + R * wp;      // iters
     int* snan = reinterpret_cast<int*>(smax + a.iters);
+    unsigned long long* stime = reinterpret_cast<unsigned long long*>(snan + a.iters);  // iters
     const int grow = blockIdx.x * R + rloc;  // global row id (batch * H)
     const bool active = rloc < R && grow < a.rows_total;
     long long goff = 0;
@@ -117,6 +120,7 @@ __global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
         const int b = grow / a.H, y = grow - b * a.H;
         goff = (long long)b * a.bstride + (long long)y * a.pitch;
     }
+    if (a.tbegin && blockIdx.x == 0 && threadIdx.x == 0) *a.tbegin = globaltimer();
     for (int k = threadIdx.x; k < a.iters; k += blockDim.x) {
         smax[k] = 0.f;
         snan[k] = 0;
@@ -217,6 +221,7 @@ __global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
             if (nan) snan[it] = 1;
         }
         __syncthreads();
+        if (threadIdx.x == 0) stime[it] = globaltimer();  // this CTA's end of iteration it
     }
     if (active) {
         for (int i = 0; i < PT; ++i) {
@@ -224,11 +229,13 @@ __global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
             if (x < W) a.u[goff + x] = ru[x];
         }
     }
+    __syncthreads();
     // publish per-iteration maxima: only values that raise the running maximum
     for (int k = threadIdx.x; k < a.iters; k += blockDim.x) {
         const unsigned b = reinterpret_cast<unsigned*>(smax)[k];
         if (a.maxchange && b > a.maxchange[k]) atomicMax(a.maxchange + k, b);
         if (a.nanflag && snan[k]) atomicOr(a.nanflag + k, 1);
+        if (a.tend) atomicMax(a.tend + k, stime[k]);
     }
 }
 
@@ -256,7 +263,7 @@ bool rowres_supported(int mx, int my, int min_dx, int min_dy, int W) {
 
 cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float* u, int pitch, int W, int H,
                           int batch, long long bstride, int iters, float eps, int clamp, unsigned* maxchange,
-                          int* nanflag, cudaStream_t st) {
+                          int* nanflag, unsigned long long* tend, unsigned long long* tbegin, cudaStream_t st) {
     RowResArgs a;
     a.f = f;
     a.u = u;
@@ -272,6 +279,8 @@ cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float
     a.clamp = clamp;
     a.maxchange = maxchange;
     a.nanflag = nanflag;
+    a.tend = tend;
+    a.tbegin = tbegin;
     // 4 columns per thread when a row fits 256 threads (more warps per row:
     // config 0 212k -> 264k Mpx*it/s), else 8
     const int PT = W <= 1024 ? 4 : 8;
@@ -291,7 +300,8 @@ cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float
     const int threads = ((rows_per_cta * nthr_row + 31) / 32) * 32;
     if (threads > 1024) return cudaErrorInvalidConfiguration;
     const int wp = (W + 3) & ~3;
-    const size_t smem = sizeof(float) * (3 * (size_t)rows_per_cta * wp + iters) + sizeof(int) * iters;
+    const size_t smem = sizeof(float) * (3 * (size_t)rows_per_cta * wp + iters) + sizeof(int) * iters +
+                        sizeof(unsigned long long) * iters;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     const int blocks = (a.rows_total + rows_per_cta - 1) / rows_per_cta;
     switch (mx * 16 + PT) {

@@ -110,6 +110,7 @@ struct SpanArgs {
     int clamp;
     unsigned* maxchange;
     int* nanflag;
+    unsigned long long* tend;
 };
 
 template <int MODE>
@@ -271,6 +272,7 @@ __device__ __forceinline__ void consume(const SpanArgs& a, const Shared& sh, int
         if (lane == 0) {
             if (bits) atomicMax(a.maxchange, bits);
             if (nan) atomicOr(a.nanflag, 1);
+            stamp_end(a.tend);
         }
     }
 }
@@ -573,6 +575,7 @@ __global__ void __launch_bounds__(32 * NTY, MINB) k_spant(const SpanArgs a) {
         const int nan = __reduce_or_sync(__activemask(), (int)isnan(csum));
         if (bits && (bits == __float_as_uint(maxd))) atomicMax(a.maxchange, bits);
         if (nan && isnan(csum)) atomicOr(a.nanflag, 1);
+        if ((threadIdx.x & 31) == (unsigned)(__ffs(__activemask()) - 1)) stamp_end(a.tend);
     }
 }
 
@@ -619,6 +622,7 @@ cudaError_t launch_shape(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
     a.clamp = e.clamp;
     a.maxchange = e.maxchange;
     a.nanflag = e.nanflag;
+    a.tend = e.tend;
     static const int nt_env = env_int("FDG_SPANS_NT");
     static const int g_env = env_int("FDG_SPANS_G");
     // Small images (<= 4.5 Mpx per launch): the tile kernel -- the marching
@@ -648,12 +652,12 @@ cudaError_t launch_shape(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
     return narrow ? launch_nt<SH, 64, 1>(a, g, e, st) : launch_nt<SH, 128, 1>(a, g, e, st);
 }
 
-int g_spans_mode = env_int("FDG_SPANS_TILE");
+std::atomic<int> g_spans_mode{env_int("FDG_SPANS_TILE")};
 
 }  // namespace
 
-void set_spans_mode(int v) { g_spans_mode = v; }
-int spans_mode() { return g_spans_mode; }
+void set_spans_mode(int v) { g_spans_mode.store(v); }
+int spans_mode() { return g_spans_mode.load(); }
 
 bool spans_supported(const DevPsf& p) {
     if (getenv("FDG_NO_SPANS")) return false;

@@ -89,6 +89,18 @@ def _image(f) -> np.ndarray:
     return a
 
 
+def _validate(a: np.ndarray, cfg: RlConfig, where: str):
+    """rl.hpp:71-84 in the reference's order (config first, then pixels) on
+    the caller's own values; float32 input is validated on the device."""
+    if a.size == 0:
+        raise _lib.FdgInvalidArgument(f"{where}: empty input image")
+    if cfg.iterations < 0:
+        raise _lib.FdgInvalidArgument(f"{where}: iterations must be >= 0")
+    if not (cfg.epsilonDiv > 0.0):
+        raise _lib.FdgInvalidArgument(f"{where}: epsilonDiv must be positive")
+    _lib.validate_image(a, where)
+
+
 def _trace(recs, n) -> RlTrace:
     return RlTrace([RlIterationRecord(recs[i].iteration, recs[i].inactive_fraction, recs[i].max_abs_change,
                                       recs[i].seconds) for i in range(n)])
@@ -101,6 +113,7 @@ def _out(a, u32):
 def rlDeconvolve(f, h, cfg: RlConfig = RlConfig(), ctx: Optional[Context] = None) -> RlResult:
     """Standard RL from u0 = f (rl.hpp:140-179)."""
     a = _image(f)
+    _validate(a, cfg, "rlDeconvolve")
     src = f32(a)
     hh, w = src.shape if src.size else (0, 0)
     u = np.empty_like(src)
@@ -118,6 +131,7 @@ def rlDeconvolveSelective(f, h, cfg: RlConfig, threshold: float, period: int = 1
     deactivation off for 0-based iterations k < thin_start (0 = reference);
     ``mask_replay`` (iterations x H x W uint8) replays recorded active masks."""
     a = _image(f)
+    _validate(a, cfg, "rlDeconvolveSelective")
     src = f32(a)
     hh, w = src.shape
     u = np.empty_like(src)
@@ -161,23 +175,41 @@ def blurImage(g, h, mode: BoundaryMode) -> np.ndarray:
 class RlSolver:
     """Device-resident RL for ``batch`` images of ``height`` x ``width``
     (fdg_solver_*).  Buffers are torch CUDA tensors (float32, last dim =
-    pitch, pitch % 4 == 0); work is issued on torch's current stream."""
+    pitch, pitch % 4 == 0).  Work is issued on torch's current stream of the
+    solver's device at the time of each call (so it is ordered with torch
+    ops and the NCCL halo exchanges torch.distributed posts there), unless
+    use_stream() pinned an explicit stream."""
 
     def __init__(self, h, cfg: RlConfig, width: int, height: int, batch: int = 1, device: int = 0,
                  ctx: Optional[Context] = None):
         self.ctx = ctx or Context(device)
+        self.device = self.ctx.device
         self.cfg = cfg
         self.width, self.height, self.batch = width, height, batch
+        self._pinned_stream = None
+        self._bound = None
         s = C.c_void_p()
         c = cfg.c()
         check(lib().fdg_solver_create(self.ctx.h, Desc(h).ref, C.byref(c), width, height, batch, C.byref(s)))
         self.h = s
 
     def use_stream(self, stream_ptr: int):
-        self.ctx.set_stream(stream_ptr)
+        """Pin every later call to this cudaStream_t."""
+        self._pinned_stream = stream_ptr
+        self._bind()
+
+    def _bind(self):
+        sp = self._pinned_stream
+        if sp is None:
+            import torch
+            sp = torch.cuda.current_stream(self.device).cuda_stream
+        if sp != self._bound:
+            self.ctx.set_stream(sp)
+            self._bound = sp
 
     def run(self, f, u, iterations: Optional[int] = None):
         """u <- f, then `iterations` RL iterations in place (device tensors)."""
+        self._bind()
         it = self.cfg.iterations if iterations is None else iterations
         pitch = f.shape[-1]
         stride = f.stride(0) if f.dim() == 3 else pitch * self.height
@@ -186,6 +218,7 @@ class RlSolver:
     def pass_(self, which: int, d_in: int, d_aux: int, d_out: int, pitch: int, image_stride: int, y0: int,
               y1: int, ylo: int, yhi: int, iteration: int):
         """One fused pass on raw device pointers (row-strip sharding)."""
+        self._bind()
         check(lib().fdg_solver_pass(self.h, which, C.c_void_p(d_in), C.c_void_p(d_aux), C.c_void_p(d_out), pitch,
                                     image_stride, y0, y1, ylo, yhi, iteration))
 
@@ -193,17 +226,20 @@ class RlSolver:
                 ylo: int, yhi: int, iteration: int):
         """One whole fused RL iteration on raw device pointers (row strips;
         engine() must be "fused")."""
+        self._bind()
         check(lib().fdg_solver_iterate(self.h, C.c_void_p(d_f), C.c_void_p(d_u_in), C.c_void_p(d_u_out), pitch,
                                        image_stride, y0, y1, ylo, yhi, iteration))
 
     def trace(self, n: Optional[int] = None):
         """[(max|du|, nan_flag)] per iteration (synchronises)."""
+        self._bind()
         n = n or max(self.cfg.iterations, 1)
         recs = (RlRecordC * n)()
         check(lib().fdg_solver_trace(self.h, recs, n))
         return [(recs[i].max_abs_change, bool(recs[i].inactive_fraction)) for i in range(n)]
 
     def reset_trace(self):
+        self._bind()
         check(lib().fdg_solver_reset_trace(self.h))
 
     def launches(self) -> int:

@@ -12,6 +12,7 @@
 #include <limits>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "fastdeconv/rl.hpp"
@@ -125,6 +126,22 @@ static void hostChecks() {
     c0.epsilonDiv = 0.0;
     check(throws_with([&] { rlDeconvolve(Image(4, 4, 1.0), Psf(makeBoxPsf(1, 1)), c0); }, "epsilonDiv"),
           "epsilonDiv <= 0 rejected");
+    // validation in double before the fp32 conversion: a tiny negative
+    // (rounds to -0.0f) is still "nonnegative"-rejected like the reference
+    bad(1, 1) = -1e-46;
+    check(throws_with([&] { rlDeconvolve(bad, Psf(makeBoxPsf(1, 1))); }, "nonnegative"),
+          "tiny negative (fp32 -0.0) rejected as negative");
+    bad(1, 1) = 1e39;
+    check(throws_with([&] { rlDeconvolve(bad, Psf(makeBoxPsf(1, 1))); }, "fp32 range"),
+          "value beyond the fp32 range refused with its own message");
+    // ConvPlan construction is host-only (dispatch), like the reference's
+    bool built = false;
+    try {
+        const ConvPlan p(Psf(makeDiscPsf(9)));
+        built = p.kind() == OperatorKind::GenericBox;
+    } catch (...) {
+    }
+    check(built, "ConvPlan constructs and resolves its operator without touching the device");
     RlConfig cg;
     cg.op = OperatorKind::GenericBox;
     check(throws_with([&] { rlDeconvolveSelective(Image(4, 4, 1.0), Psf(makeDiscPsf(3)), cg, 0.1); },
@@ -265,6 +282,51 @@ static void deviceChecks() {
     const Image s1 = rlStep(fb2, fb2, Psf(makeBoxPsf(3, 3)), cn2);
     const Image s2 = detail::rlStepPlanned(fb2, fb2, fwd, adj, cn2);
     check(identical(s1, s2), "rlStepPlanned == rlStep");
+    // rlStepPlanned honours the caller's adjoint plan: with an asymmetric
+    // PSF and the FORWARD plan passed as "adjoint" the step is
+    // u * (h (x) (f / (h (x) u))), not rlStep's u * (h* (x) ...)
+    {
+        const Psf ha(DensePsf(3, 1, 1, 0, {1.0, 2.0, 5.0}));
+        const ConvPlan fa(ha, OperatorKind::Naive);
+        const Image u0 = randomImage(rng, 40, 24, 1.0, 2.0), f0 = randomImage(rng, 40, 24, 1.0, 2.0);
+        const Image sp = detail::rlStepPlanned(u0, f0, fa, fa, cn2);
+        const Image st = rlStep(u0, f0, ha, cn2);
+        const Image v = oracleConv(u0, ha, OperatorKind::Naive);
+        Image q(40, 24);
+        for (size_t i = 0; i < q.data().size(); ++i) q.data()[i] = f0.data()[i] / std::max(v.data()[i], 1e-8);
+        const Image c = oracleConv(q, ha, OperatorKind::Naive);
+        Image ex(40, 24);
+        for (size_t i = 0; i < ex.data().size(); ++i) ex.data()[i] = std::max(c.data()[i] * u0.data()[i], 0.0);
+        check(maxRel(sp, ex) <= 1e-5 && maxRel(st, ex) > 1e-3,
+              "rlStepPlanned uses the caller's adjoint plan (max-rel " + std::to_string(maxRel(sp, ex)) + ")");
+    }
+    // one ConvPlan shared by several threads (each on its own context)
+    {
+        const ConvPlan shared(Psf(makeDiscPsf(9)));
+        std::vector<Image> in, seq, par(6);
+        for (int t = 0; t < 6; ++t) in.push_back(randomImage(rng, 300 + 16 * t, 200 + 8 * t));
+        for (int t = 0; t < 6; ++t) seq.push_back(shared.apply(in[t]));
+        std::vector<std::thread> th;
+        for (int t = 0; t < 6; ++t)
+            th.emplace_back([&, t] {
+                for (int rep = 0; rep < 3; ++rep) par[t] = shared.apply(in[t]);
+            });
+        for (auto& x : th) x.join();
+        bool same = true;
+        for (int t = 0; t < 6; ++t) same &= identical(par[t], seq[t]);
+        check(same, "one ConvPlan applied concurrently from 6 threads == sequential results");
+    }
+    // a plan built on a worker thread stays valid after that thread exits
+    {
+        std::unique_ptr<ConvPlan> p;
+        std::thread([&] {
+            p = std::make_unique<ConvPlan>(Psf(makeBoxPsf(5, 3)));
+            (void)p->engine();  // device representation built on this thread's context
+        }).join();
+        const Image img = randomImage(rng, 64, 48);
+        check(maxRel(p->apply(img), oracleConv(img, Psf(makeBoxPsf(5, 3)), p->kind())) <= 2e-6,
+              "plan used after its creating thread exited");
+    }
 }
 
 int main(int argc, char** argv) {

@@ -116,6 +116,41 @@ def test_validation_without_device():
         rlDeconvolveSelective(f, makeDiscPsf(3), RlConfig(op=K.GenericBox), 0.1)
 
 
+def test_validation_in_double_before_fp32():
+    """rl.hpp:78-83 on the caller's float64 values: a tiny negative that
+    rounds to -0.0f is still rejected, the first offending pixel decides the
+    message, and values beyond the fp32 range are refused explicitly."""
+    f = np.ones((5, 7), np.float64)
+    bad = f.copy()
+    bad[2, 3] = -1e-46
+    assert np.float32(bad[2, 3]) == 0.0
+    with pytest.raises(ValueError, match="must be nonnegative"):
+        rlDeconvolve(bad, makeBoxPsf(1, 1))
+    with pytest.raises(ValueError, match="must be nonnegative"):
+        rlDeconvolveSelective(bad, makeBoxPsf(1, 1), RlConfig(), 0.1)
+    bad[4, 0] = np.inf  # later in row-major order: the negative wins
+    with pytest.raises(ValueError, match="must be nonnegative"):
+        rlDeconvolve(bad, makeBoxPsf(1, 1))
+    bad[0, 1] = np.nan  # earlier: non-finite wins
+    with pytest.raises(ValueError, match="non-finite"):
+        rlDeconvolve(bad, makeBoxPsf(1, 1))
+    big = f.copy()
+    big[1, 1] = 1e39
+    with pytest.raises(ValueError, match="fp32 range"):
+        rlDeconvolve(big, makeBoxPsf(1, 1))
+    # config errors come first, like validateRlInputs
+    with pytest.raises(ValueError, match="iterations must be >= 0"):
+        rlDeconvolve(bad, makeBoxPsf(1, 1), RlConfig(iterations=-1))
+
+
+def test_convplan_is_host_only_until_applied():
+    from paper_1304_7211_b200 import ConvPlan
+    p = ConvPlan(makeDiscPsf(9))
+    assert p.kind() == K.GenericBox
+    p = ConvPlan(makeBoxPsf(15, 15), K.Box2dSliding)
+    assert p.kind() == K.Box2dSliding
+
+
 @pytest.mark.skipif(_lib.device_available(), reason="checks the no-device behaviour")
 def test_no_cpu_fallback():
     with pytest.raises(_lib.FdgError, match="no CUDA"):
