@@ -194,6 +194,8 @@ struct fdg_solver {
     DevBuf<int> nanflag;
     // %globaltimer stamps: [0] start of the last run, [k + 1] end of iteration k
     DevBuf<unsigned long long> tstamp;
+    DevBuf<unsigned long long> tdur;  // row-resident runs: per-iteration durations summed over CTAs
+    bool last_rowres = false;         // engine of the last run (trace seconds)
     // CUDA graph of one full fdg_solver_run (replayed while the arguments and
     // the engine options it was captured under match)
     cudaGraphExec_t gexec = nullptr;
@@ -219,6 +221,7 @@ struct fdg_solver {
         maxchange.release();
         nanflag.release();
         tstamp.release();
+        tdur.release();
         q.release();
         if (holds_ref) ctx_release(ctx);
     }
@@ -475,12 +478,15 @@ bool use_rowres(const fdg_plan* pl, int W) {
 }
 
 // Trace slots of a loop of `iters` iterations: per-iteration max|du| (float
-// bits), NaN flag, and %globaltimer stamps ([0] = start, [k + 1] = end of
-// iteration k).  Any pointer may be null.
+// bits), NaN flag, %globaltimer stamps ([0] = start, [k + 1] = end of
+// iteration k) and, for the row-resident engine whose CTAs run their
+// iterations out of phase, the per-iteration duration summed over CTAs.
+// Any pointer may be null.
 struct TraceSlots {
     unsigned* mc = nullptr;
     int* nf = nullptr;
     unsigned long long* ts = nullptr;
+    unsigned long long* dur = nullptr;
     unsigned* mc_at(int k) const { return mc ? mc + k : nullptr; }
     int* nf_at(int k) const { return nf ? nf + k : nullptr; }
     unsigned long long* end_at(int k) const { return ts ? ts + 1 + k : nullptr; }
@@ -491,7 +497,7 @@ int run_rowres(fdg_ctx* ctx, const fdg_plan* pl, const float* f, float* u, int p
     const DevPsf& d = pl->dev;
     cudaError_t r = launch_rowres(d.mx, d.min_dx, d.scale, f, u, pitch, W, H, batch, bstride, iters,
                                   (float)cfg->epsilon_div, cfg->clamp_nonnegative, tr.mc, tr.nf, tr.end_at(0), tr.ts,
-                                  st);
+                                  tr.dur, st);
     if (r != cudaSuccess) return cuda_err(r, "row-resident RL launch");
     ctx->launches += 1;
     return FDG_OK;
@@ -529,6 +535,25 @@ Geom whole(const float* in, float* out, int pitch, int W, int H, int batch = 1, 
     g.batch = batch;
     g.bstride = bstride;
     return g;
+}
+
+// Per-iteration seconds from the trace stamps: stamp differences, or for a
+// row-resident run (dur != empty) the run time split in proportion to the
+// summed per-CTA iteration durations.
+std::vector<double> trace_seconds(const std::vector<unsigned long long>& ts, const std::vector<unsigned long long>& dur,
+                                  int n) {
+    std::vector<double> sec(n, 0.0);
+    if (!dur.empty()) {
+        double tot = 0.0;
+        for (int k = 0; k < n; ++k) tot += (double)dur[k];
+        const double run = ts[0] && ts[n] > ts[0] ? (double)(ts[n] - ts[0]) * 1e-9 : 0.0;
+        if (tot > 0.0)
+            for (int k = 0; k < n; ++k) sec[k] = run * (double)dur[k] / tot;
+        return sec;
+    }
+    for (int k = 0; k < n; ++k)
+        if (ts[k] && ts[k + 1] > ts[k]) sec[k] = (double)(ts[k + 1] - ts[k]) * 1e-9;
+    return sec;
 }
 
 // Every device entry point holds its context's lock and runs on the
@@ -1062,6 +1087,8 @@ int solver_create(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* c
     CK(s->maxchange.ensure(s->ntrace));
     CK(s->nanflag.ensure(s->ntrace));
     CK(s->tstamp.ensure(s->ntrace + 1));
+    CK(s->tdur.ensure(s->ntrace));
+    CK(cudaMemset(s->tdur.p, 0, sizeof(unsigned long long) * s->ntrace));
     CK(cudaMemset(s->maxchange.p, 0, sizeof(unsigned) * s->ntrace));
     CK(cudaMemset(s->nanflag.p, 0, sizeof(int) * s->ntrace));
     CK(cudaMemset(s->tstamp.p, 0, sizeof(unsigned long long) * (s->ntrace + 1)));
@@ -1074,10 +1101,13 @@ int solver_reset_trace(fdg_solver* s) {
     CK(cudaMemsetAsync(s->maxchange.p, 0, sizeof(unsigned) * s->ntrace, st));
     CK(cudaMemsetAsync(s->nanflag.p, 0, sizeof(int) * s->ntrace, st));
     CK(cudaMemsetAsync(s->tstamp.p, 0, sizeof(unsigned long long) * (s->ntrace + 1), st));
+    CK(cudaMemsetAsync(s->tdur.p, 0, sizeof(unsigned long long) * s->ntrace, st));
     return FDG_OK;
 }
 
-TraceSlots solver_slots(const fdg_solver* s) { return TraceSlots{s->maxchange.p, s->nanflag.p, s->tstamp.p}; }
+TraceSlots solver_slots(const fdg_solver* s) {
+    return TraceSlots{s->maxchange.p, s->nanflag.p, s->tstamp.p, s->tdur.p};
+}
 
 int solver_pass(fdg_solver* s, int pass, const float* d_in, const float* d_aux, float* d_out, int pitch,
                 long long image_stride, int y0, int y1, int ylo, int yhi, int iteration) {
@@ -1133,6 +1163,8 @@ int solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long
         CK(cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming));
     }
     const int opts = options_key();
+    const bool rowres = use_rowres(s->fwd.get(), s->W) && iterations > 0 && iterations <= s->ntrace;
+    s->last_rowres = rowres;
     if (!no_graph && s->gexec && s->g_f == d_f && s->g_u == d_u && s->g_pitch == pitch && s->g_stride == stride &&
         s->g_iters == iterations && s->g_opts == opts) {
         CK(cudaEventRecord(s->ev_in, user));
@@ -1144,7 +1176,6 @@ int solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long
         return FDG_OK;
     }
     const uint64_t before = ctx->launches;
-    const bool rowres = use_rowres(s->fwd.get(), s->W) && iterations > 0 && iterations <= s->ntrace;
     const bool fused = !rowres && use_fused(s->fwd.get());
     const TraceSlots tr = solver_slots(s);
     auto issue = [&]() -> int {
@@ -1218,18 +1249,19 @@ int solver_trace(fdg_solver* s, int n, std::vector<float>* mc, std::vector<int>*
     cudaStream_t st = s->ctx->stream;
     n = std::min(n, s->ntrace);
     std::vector<unsigned> m(n);
-    std::vector<unsigned long long> ts(n + 1);
+    std::vector<unsigned long long> ts(n + 1), dur;
     nf->assign(n, 0);
     CK(cudaMemcpyAsync(m.data(), s->maxchange.p, sizeof(unsigned) * n, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(nf->data(), s->nanflag.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(ts.data(), s->tstamp.p, sizeof(unsigned long long) * (n + 1), cudaMemcpyDeviceToHost, st));
+    if (s->last_rowres) {
+        dur.resize(n);
+        CK(cudaMemcpyAsync(dur.data(), s->tdur.p, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, st));
+    }
     CK(cudaStreamSynchronize(st));
     mc->resize(n);
-    sec->assign(n, 0.0);
-    for (int k = 0; k < n; ++k) {
-        std::memcpy(&(*mc)[k], &m[k], sizeof(float));
-        if (ts[k] && ts[k + 1] > ts[k]) (*sec)[k] = (double)(ts[k + 1] - ts[k]) * 1e-9;
-    }
+    for (int k = 0; k < n; ++k) std::memcpy(&(*mc)[k], &m[k], sizeof(float));
+    *sec = trace_seconds(ts, dur, n);
     return FDG_OK;
 }
 
@@ -1320,6 +1352,7 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     CK(ctx->tr_max.ensure(iters + 1));
     CK(ctx->tr_nan.ensure(iters + 1));
     CK(ctx->tr_time.ensure(iters + 2));
+    CK(ctx->tr_inact.ensure(iters + 1));
     float *df = ctx->a.p, *du = ctx->b.p, *dq = ctx->c.p;
     pt.mark("alloc");
     if ((st = h2d(ctx->stg, df, pitch, f, W, H, s))) return st;
@@ -1347,10 +1380,11 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
         return FDG_OK;
     }
     // uncached (FDG_NO_RL_CACHE, or 0 iterations): launch the loop directly
-    const TraceSlots tr{ctx->tr_max.p, ctx->tr_nan.p, ctx->tr_time.p};
+    const TraceSlots tr{ctx->tr_max.p, ctx->tr_nan.p, ctx->tr_time.p, ctx->tr_inact.p};
     CK(cudaMemsetAsync(tr.mc, 0, sizeof(unsigned) * (iters + 1), s));
     CK(cudaMemsetAsync(tr.nf, 0, sizeof(int) * (iters + 1), s));
     CK(cudaMemsetAsync(tr.ts, 0, sizeof(unsigned long long) * (iters + 2), s));
+    CK(cudaMemsetAsync(tr.dur, 0, sizeof(unsigned long long) * (iters + 1), s));
     CK(cudaMemcpyAsync(du, df, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
     const bool rowres = use_rowres(fwd.get(), W) && iters > 0;
     if (rowres) {
@@ -1394,19 +1428,20 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     if ((st = d2h(ctx->stg, u_out, du, pitch, W, H, s))) return st;
     std::vector<unsigned> hmc(iters + 1);
     std::vector<int> hnf(iters + 1);
-    std::vector<unsigned long long> hts(iters + 2);
+    std::vector<unsigned long long> hts(iters + 2), hdur(rowres ? iters : 0);
     CK(cudaMemcpyAsync(hmc.data(), tr.mc, sizeof(unsigned) * (iters + 1), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hnf.data(), tr.nf, sizeof(int) * (iters + 1), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hts.data(), tr.ts, sizeof(unsigned long long) * (iters + 2), cudaMemcpyDeviceToHost, s));
+    if (rowres) CK(cudaMemcpyAsync(hdur.data(), tr.dur, sizeof(unsigned long long) * iters, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     pt.mark("d2h");
+    const std::vector<double> sec = trace_seconds(hts, hdur, iters);
     for (int k = 0; k < iters; ++k) {
         if (hnf[k]) return set_err(FDG_ENAN, "rlDeconvolve: NaN in iterate at iteration " + std::to_string(k + 1));
         if (trace) {
             float m;
             std::memcpy(&m, &hmc[k], sizeof m);
-            const double sec = hts[k] && hts[k + 1] > hts[k] ? (double)(hts[k + 1] - hts[k]) * 1e-9 : 0.0;
-            trace[k] = {k + 1, 0.0, (double)m, sec};
+            trace[k] = {k + 1, 0.0, (double)m, sec[k]};
         }
     }
     return FDG_OK;

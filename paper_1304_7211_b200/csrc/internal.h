@@ -132,7 +132,8 @@ bool rect_supported(int mx);
 bool rowres_supported(int mx, int my, int min_dx, int min_dy, int W);
 cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float* u, int pitch, int W, int H,
                           int batch, long long bstride, int iters, float eps, int clamp, unsigned* maxchange,
-                          int* nanflag, unsigned long long* tend, unsigned long long* tbegin, cudaStream_t st);
+                          int* nanflag, unsigned long long* tend, unsigned long long* tbegin, unsigned long long* tdur,
+                          cudaStream_t st);
 // Whole RL iteration in one pass for the centred 15x15 box (kernels_fused.cu):
 // u_out = max(box*(f / max(box(u_in), eps)) * u_in, 0); u_in != u_out.
 bool fused_supported(int mx, int my, int min_dx, int min_dy);

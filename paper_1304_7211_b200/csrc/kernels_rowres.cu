@@ -38,6 +38,7 @@ struct RowResArgs {
     int* nanflag;         // [iters]
     unsigned long long* tend;  // [iters] %globaltimer at the end of iteration k (max over CTAs)
     unsigned long long* tbegin;  // start stamp of the run (block 0)
+    unsigned long long* tdur;    // [iters] sum over CTAs of the iteration's duration (ns)
 };
 
 template <int N>
@@ -120,7 +121,8 @@ __global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
         const int b = grow / a.H, y = grow - b * a.H;
         goff = (long long)b * a.bstride + (long long)y * a.pitch;
     }
-    if (a.tbegin && blockIdx.x == 0 && threadIdx.x == 0) *a.tbegin = globaltimer();
+    const unsigned long long t0 = globaltimer();
+    if (a.tbegin && blockIdx.x == 0 && threadIdx.x == 0) *a.tbegin = t0;
     for (int k = threadIdx.x; k < a.iters; k += blockDim.x) {
         smax[k] = 0.f;
         snan[k] = 0;
@@ -236,6 +238,9 @@ __global__ void __launch_bounds__(256, 2) k_rowres(const RowResArgs a) {
         if (a.maxchange && b > a.maxchange[k]) atomicMax(a.maxchange + k, b);
         if (a.nanflag && snan[k]) atomicOr(a.nanflag + k, 1);
         if (a.tend) atomicMax(a.tend + k, stime[k]);
+        // CTAs run their iterations out of phase (several waves): the
+        // per-iteration share of the run is the summed per-CTA duration
+        if (a.tdur) atomicAdd(a.tdur + k, stime[k] - (k ? stime[k - 1] : t0));
     }
 }
 
@@ -263,7 +268,8 @@ bool rowres_supported(int mx, int my, int min_dx, int min_dy, int W) {
 
 cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float* u, int pitch, int W, int H,
                           int batch, long long bstride, int iters, float eps, int clamp, unsigned* maxchange,
-                          int* nanflag, unsigned long long* tend, unsigned long long* tbegin, cudaStream_t st) {
+                          int* nanflag, unsigned long long* tend, unsigned long long* tbegin, unsigned long long* tdur,
+                          cudaStream_t st) {
     RowResArgs a;
     a.f = f;
     a.u = u;
@@ -281,6 +287,7 @@ cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float
     a.nanflag = nanflag;
     a.tend = tend;
     a.tbegin = tbegin;
+    a.tdur = tdur;
     // 4 columns per thread when a row fits 256 threads (more warps per row:
     // config 0 212k -> 264k Mpx*it/s), else 8
     const int PT = W <= 1024 ? 4 : 8;
