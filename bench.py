@@ -50,44 +50,61 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    every 10 ms in a thread (an nvidia-smi loop needs ~0.3 s to start and
+    missed sub-second runs), plus one sample at start() and at stop()."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, period_s=0.01):
         self.index = index
+        self.period = period_s
         self.rows = []
-        self.proc = None
+        self._stop = threading.Event()
+        self._th = None
+        self._h = None
+        self._max = None
+
+    def _sample(self):
+        import pynvml
+        try:
+            sm = pynvml.nvmlDeviceGetClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            try:
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+            self.rows.append((sm, r))
+        except Exception:
+            pass
+
+    def _loop(self):
+        while not self._stop.wait(self.period):
+            self._sample()
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._read, daemon=True).start()
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._sample()
+            self._th = threading.Thread(target=self._loop, daemon=True)
+            self._th.start()
         except Exception:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+            self._h = None
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except Exception:
-                self.proc.kill()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        if self._h is not None:
+            self._stop.set()
+            if self._th:
+                self._th.join(1.0)
+            self._sample()
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for _, bits in self.rows for b, name in self.REASONS.items() if bits & b})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self._max,
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml (10 ms)"}
 
 
 def dist_env():
@@ -98,58 +115,127 @@ def dist_env():
 
 
 # --------------------------------------------------------------- reference
-def run_reference(args, cfg, world, rank):
+WORKLOAD_KEYS = ("workload", "width", "height", "batch", "psf", "op", "iterations")
+
+
+def workload_config(cfg, iterations=None):
+    """The `config` object of both arms: the workload only (engine details
+    go to `engine_info`), so the driver sees identical configs."""
+    return {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "batch": cfg.batch,
+            "psf": cfg.psf, "op": cfg.op, "iterations": iterations or cfg.iterations}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# single-core cost of the reference per px*it on the B200 host (r01), by
+# reference operator (sizes the bounded samples)
+REF_US_PER_PXIT = {"box1d-sliding": 0.011, "box1d-cumul": 0.012, "box2d-sliding": 0.016, "box2d-cumul": 0.014,
+                   "generic-box": 0.08, "naive": 1.7}
+REF_OPS = {"naive": 0, "list": 1, "generic-box": 2, "box2d-sliding": 3, "box2d-cumul": 4, "box1d-sliding": 5,
+           "box1d-cumul": 6}
+AUTO_OP = {"line15": "box1d-cumul", "line31": "box1d-cumul", "box15x15": "box2d-cumul", "disc10": "generic-box",
+           "oblique21": "generic-box", "gauss31": "naive"}  # dispatch(Auto), convolve.hpp:628-633
+
+
+def reference_sample(cfg, op_name=None, budget_s=10.0):
+    """(rows per strip, iterations): about `budget_s` of single-core
+    reference work per thread at the config's width (full-width strips: the
+    per-pixel cost is what the metric needs; BASELINE.md 3 times 3-5
+    iterations of the long configs)."""
+    per_px_it_us = REF_US_PER_PXIT[op_name or cfg.op]
+    px_it = budget_s * 1e6 / per_px_it_us
+    iters = cfg.iterations
+    rows = int(px_it / iters / cfg.width)
+    if rows < 32:  # expensive operators / huge rows: fewer iterations instead of thinner strips
+        rows = 32
+        iters = max(2, int(px_it / rows / cfg.width))
+    return min(rows, cfg.height), min(iters, cfg.iterations)
+
+
+def ref_rate(cfg, op_name, threads, budget_s, pin_core=None):
+    """Mpx*it/s of the reference rlDeconvolve(op) on `threads` independent
+    full-width strips (one per thread; `pin_core`: the calling thread and
+    its strip thread pinned to that core), and the sample description."""
     from oracle import pyoracle as O
     from paper_1304_7211_b200 import workloads as W
+    psf = W.make_psf(cfg.psf)
+    strip_rows, iters = reference_sample(cfg, op_name, budget_s)
+    rows = min(cfg.height, strip_rows + 64)
+    _, f = W.make_input(cfg, cfg.width, rows)
+    prev = os.sched_getaffinity(0) if pin_core is not None else None
+    try:
+        if pin_core is not None:
+            os.sched_setaffinity(0, {pin_core})
+        secs, pxit = O.ref_bench_strips(f.astype(np.float64), psf, REF_OPS[op_name], iters, threads, strip_rows)
+    finally:
+        if prev is not None:
+            os.sched_setaffinity(0, prev)
+    sample = (f"reference rlDeconvolve({op_name}) x {threads} independent {strip_rows}x{cfg.width} strips, "
+              f"{iters} iterations, {secs:.1f} s" + (f", pinned to core {pin_core}" if pin_core is not None else ""))
+    return pxit / secs / 1e6, sample
+
+
+def run_reference(args, cfg, world, rank):
+    """The reference's own CPU implementation of the path (oracle/_ref, the
+    unmodified headers) on all host threads of this box, rank 0 only."""
+    from oracle import pyoracle as O
 
     if rank != 0:
         return 0
-    psf = W.make_psf(cfg.psf)
-    op = {"box1d-sliding": O.BOX1D_SLIDING, "box2d-sliding": O.BOX2D_SLIDING, "generic-box": O.GENERIC_BOX,
-          "naive": O.NAIVE}[cfg.op]
-    threads = os.cpu_count() or 1
-    strip_rows, iters = reference_sample(cfg)
-    rows = min(cfg.height, strip_rows + 64)  # threads run independent strips of this sample
-    _, f = W.make_input(cfg, cfg.width, rows)
-    f64 = f.astype(np.float64)
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfdref.so not built"}))
         return 0
-    vals = []
+    threads = len(os.sched_getaffinity(0)) or 1
+    vals, sample = [], ""
     for i in range(args.warmup + args.steps):
-        secs, pxit = O.ref_bench_strips(f64, psf, op, iters, threads, strip_rows)
+        v, sample = ref_rate(cfg, cfg.op, threads, budget_s=5.0)
         if i >= args.warmup:
-            vals.append(pxit / secs / 1e6)
+            vals.append(v)
     value = statistics.median(vals)
-    sample = (f"{threads} threads x reference rlDeconvolve({cfg.op}) on independent {strip_rows}-row x "
-              f"{cfg.width} strips, {iters} iterations each (single-threaded library, one strip per core)")
+    sample += f"; host {cpu_model()}, nproc {os.cpu_count()}"
     line = {"metric": "RL Mpixel*iterations/s", "value": value, "unit": "Mpx*it/s", "impl": "reference",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "ms_per_step": None, "scaling": "strong" if cfg.batch == 1 else "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "batch": cfg.batch,
-                       "psf": cfg.psf, "op": cfg.op, "iterations": cfg.iterations},
+            "dtype": "f64", "data": "synthetic (seeded BASELINE generator)",
+            "config": workload_config(cfg, args.iterations),
             "cpu_baseline": {"value": value, "unit": "Mpx*it/s", "cores": threads, "kind": "reference",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model(), "nproc": os.cpu_count()},
             "e2e": {"value": value, "unit": "Mpx*it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
 
-def reference_sample(cfg):
-    """(rows per strip, iterations): ~10 s of single-core reference work per
-    thread, at the config's width, on a strip short enough that generating
-    its input takes well under a second."""
-    # single-core reference cost per px*it measured on the B200 host (r01)
-    per_px_it_us = {"box1d-sliding": 0.011, "box2d-sliding": 0.016, "generic-box": 0.08, "naive": 1.7}[cfg.op]
-    budget = 10.0e6  # us per thread
-    px_it = budget / per_px_it_us
-    iters = cfg.iterations
-    rows = int(px_it / iters / cfg.width)
-    if rows < 32:  # expensive operators: fewer iterations instead of thinner strips
-        rows = 32
-        iters = max(2, int(px_it / rows / cfg.width))
-    return min(rows, cfg.height), min(iters, cfg.iterations)
+def cpu_baseline(cfg):
+    """the reference (oracle/_ref) single-threaded as designed,
+    pinned to one core, with the config's named operator (the headline
+    value) and the Auto-dispatched one; plus all host threads on
+    independent strips as a separately labelled aggregate.  ~20 s total."""
+    try:
+        from oracle import pyoracle as O
+        if not O.ref_available():
+            return None
+        core = sorted(os.sched_getaffinity(0))[-1]
+        named, s_named = ref_rate(cfg, cfg.op, 1, budget_s=6.0, pin_core=core)
+        auto_op = AUTO_OP[cfg.psf]
+        auto, s_auto = ref_rate(cfg, auto_op, 1, budget_s=6.0, pin_core=core)
+        threads = len(os.sched_getaffinity(0)) or 1
+        agg, s_agg = ref_rate(cfg, cfg.op, threads, budget_s=5.0)
+        return {"value": named, "unit": "Mpx*it/s", "cores": 1, "kind": "reference",
+                "sample": s_named + " (1 core of " + str(os.cpu_count()) + ")",
+                "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+                "auto_operator": {"op": auto_op, "value": auto, "cores": 1, "sample": s_auto},
+                "all_threads": {"value": agg, "cores": threads, "sample": s_agg}}
+    except Exception as e:  # the baseline is reported, never required
+        return {"value": None, "error": str(e)}
 
 
 # ---------------------------------------------------------------- our path
@@ -340,13 +426,14 @@ def run_ours(args, cfg, world, rank, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if cfg.batch == 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded BASELINE generator)",
-            "config": {"workload": cfg.name, "width": W_, "height": H_, "batch": cfg.batch, "psf": cfg.psf,
-                       "op": cfg.op, "iterations": iters, "engine": engine,
-                       "parallelism": (f"rowstrip{world}" + ("-fused" if fused_strips else "")) if cfg.batch == 1
-                       else f"image-shard{world}",
-                       "l2": "working set 3 planes >> 126 MB L2 (no flush needed)" if W_ * H_ * 12 * nimg > 4e8
-                       else "working set L2-resident",
-                       "setup_s": round(setup_s, 2)},
+            "config": workload_config(cfg, iters),
+            "engine_info": {"engine": engine,
+                            "parallelism": (f"rowstrip{world}" + ("-fused" if fused_strips else ""))
+                            if cfg.batch == 1 else f"image-shard{world}",
+                            "l2": "working set 3 planes >> 126 MB L2 (no flush needed)" if W_ * H_ * 12 * nimg > 4e8
+                            else "working set L2-resident (no flush: the RL loop re-reads its own planes)",
+                            "setup_s": round(setup_s, 2)},
+            "per_gpu_value": value / world,
             "roofline": roof if roof else {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": kernel_desc, "engine": engine, "kernel_ms": kern_ms,
@@ -391,27 +478,6 @@ def make_input_gpu(cfg, psf, dev, image=0):
     f = torch.clamp_min(bd + noise, 1e-6)
     torch.cuda.synchronize(dev)
     return f
-
-
-def cpu_baseline(cfg):
-    try:
-        from oracle import pyoracle as O
-        from paper_1304_7211_b200 import workloads as W
-        if not O.ref_available():
-            return None
-        psf = W.make_psf(cfg.psf)
-        op = {"box1d-sliding": O.BOX1D_SLIDING, "box2d-sliding": O.BOX2D_SLIDING, "generic-box": O.GENERIC_BOX,
-              "naive": O.NAIVE}[cfg.op]
-        threads = os.cpu_count() or 1
-        strip_rows, iters = reference_sample(cfg)
-        rows = min(cfg.height, strip_rows + 64)
-        _, f = W.make_input(cfg, cfg.width, rows)
-        secs, pxit = O.ref_bench_strips(f.astype(np.float64), psf, op, iters, threads, strip_rows)
-        return {"value": pxit / secs / 1e6, "unit": "Mpx*it/s", "cores": threads, "kind": "reference",
-                "sample": f"{threads} threads x reference rlDeconvolve({cfg.op}), {strip_rows}x{cfg.width} strips, "
-                          f"{iters} iterations, {secs:.1f} s"}
-    except Exception as e:  # the baseline is reported, never required
-        return {"value": None, "error": str(e)}
 
 
 def run_thinned(args, cfg, world, rank, local):
@@ -469,9 +535,9 @@ def run_thinned(args, cfg, world, rank, local):
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": loop_s * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded BASELINE generator)",
-            "config": {"workload": f"cfg3-{args.thin}", "width": cfg.width, "height": cfg.height, "psf": cfg.psf,
-                       "op": "naive (masked dense)", "iterations": iters, "threshold": thr, "period": 10,
-                       "thin_start": 20, "masks": "free-running on the GPU", "engine": "dense (masked)"},
+            "config": dict(workload_config(cfg, iters), workload=f"cfg3-{args.thin}"),
+            "engine_info": {"op": "naive (masked dense)", "threshold": thr, "period": 10, "thin_start": 20,
+                            "masks": "free-running on the GPU", "engine": "dense (masked)"},
             "active_fraction_it21_on": act, "active_px_rate_mpxit": value * a_mean,
             "unthinned_value": pxit / un_s / 1e6, "speedup_vs_unthinned": un_s / loop_s,
             "roofline": {"bound": "fp32", "achieved": tf, "peak": FP32_TFLOPS_MEASURED, "unit": "TFLOP/s",
@@ -486,6 +552,52 @@ def run_thinned(args, cfg, world, rank, local):
     return 0
 
 
+def run_dry(args, cfg, world, rank):
+    """--dry-run: the N-rank plumbing without a GPU (gloo): every rank
+    reports its row strip (or image share) and rank 0 prints the table --
+    proves that --gpus N starts N ranks with the sharding bench.py uses."""
+    import torch.distributed as dist
+
+    from paper_1304_7211_b200 import sharded as S, workloads as W
+    if world > 1:
+        dist.init_process_group("gloo")
+    psf = W.make_psf(cfg.psf)
+    if cfg.batch == 1:
+        halo = S.fused_halo(psf) if cfg.psf == "box15x15" else S.psf_halo(psf)
+        s = S.strip_of(cfg.height, world, rank, halo if world > 1 else 0)
+        mine = {"rank": rank, "rows": [s.r0, s.r0 + s.core], "halo": s.halo}
+    else:
+        sh = S.batch_share(cfg.batch, world, rank)
+        mine = {"rank": rank, "images": [sh.start, sh.stop]}
+    table = [None] * world
+    if world > 1:
+        dist.all_gather_object(table, mine)
+    else:
+        table = [mine]
+    if rank == 0:
+        halo_bytes = 0
+        if cfg.batch == 1 and world > 1:  # per iteration, both directions, all inner edges
+            halo_bytes = 2 * (world - 1) * table[0]["halo"] * cfg.width * 4
+        print(json.dumps({"dry_run": True, "n_gpus": world, "config": workload_config(cfg, args.iterations),
+                          "shards": table, "halo_bytes_per_iteration": halo_bytes}))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def relaunch(n):
+    """`bench.py --gpus N` outside torchrun: re-exec under
+    torch.distributed.run with N local ranks (the driver's own launch)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -497,10 +609,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--thin", default=None, choices=["active50", "active25"],
                     help="config 3 thinned (selective RL) at the calibrated active fraction")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="rank plumbing only (gloo, no GPU): print each rank's shard")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args.gpus)
     from paper_1304_7211_b200 import workloads as W
     cfg = W.CONFIGS[args.config]
     world, rank, local = dist_env()
+    if args.dry_run:
+        return run_dry(args, cfg, world, rank)
     if args.impl == "reference":
         return run_reference(args, cfg, world, rank)
     if args.thin:
