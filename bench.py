@@ -344,7 +344,9 @@ def run_ours(args, cfg, world, rank, local):
     # is the step time over the launches (incl. halo exchanges when world > 1)
     # (row strips on several ranks run the two-pass solver passes)
     engine = solver.engine() if world == 1 or cfg.batch > 1 or fused_strips else ConvPlan(psf, op).engine()
-    per_step = max(1, round(launches / max(1, args.steps) / max(1, world)))
+    # launches of the dominant kernel per step (the step also has one tiny
+    # start-stamp kernel for the per-iteration trace)
+    per_step = {"fused": iters, "rowres": 1}.get(engine, 2 * iters)
     kern_ms = ms_step / per_step
     pxit_per_launch = px_local * iters / per_step
     # algorithmic bytes: SURVEY 8d's canonical 24 B/px*it (two passes x (2

@@ -190,6 +190,7 @@ struct fdg_solver {
     int W = 0, H = 0, batch = 1;
     int ntrace = 0;
     DevBuf<float> q;
+    DevBuf<float> uh;  // fused engine: two haloed u planes (ping-pong between iterations)
     DevBuf<unsigned> maxchange;
     DevBuf<int> nanflag;
     // %globaltimer stamps: [0] start of the last run, [k + 1] end of iteration k
@@ -223,6 +224,7 @@ struct fdg_solver {
         tstamp.release();
         tdur.release();
         q.release();
+        uh.release();
         if (holds_ref) ctx_release(ctx);
     }
 };
@@ -510,13 +512,22 @@ bool use_fused(const fdg_plan* pl) {
     return d.engine == ENG_RECT && fused_supported(d.mx, d.my, d.min_dx, d.min_dy);
 }
 
+// Haloed u planes of the fused loop (see launch_fused)
+struct HaloPlanes {
+    float* p[2] = {nullptr, nullptr};  // column 0 of each plane
+    int pitch = 0;
+    long long stride = 0;  // elements between images
+};
+
 int run_fused(fdg_ctx* ctx, const fdg_plan* pl, const float* u_in, const float* f, float* u_out, int pitch, int W,
               int H, int batch, long long bstride, const fdg_rl_config* cfg, unsigned* mc, int* nf,
-              unsigned long long* te, cudaStream_t st, int y0 = 0, int y1 = -1, int ylo = 0, int yhi = -1) {
+              unsigned long long* te, cudaStream_t st, int y0 = 0, int y1 = -1, int ylo = 0, int yhi = -1,
+              const HaloPlanes* hp = nullptr, int halo_in = 0, int halo_out = 0) {
     if (y1 < 0) y1 = H;
     if (yhi < 0) yhi = H - 1;
     cudaError_t r = launch_fused(u_in, f, u_out, pitch, W, y0, y1, ylo, yhi, batch, bstride, pl->dev.scale,
-                                 (float)cfg->epsilon_div, cfg->clamp_nonnegative, mc, nf, te, st);
+                                 (float)cfg->epsilon_div, cfg->clamp_nonnegative, mc, nf, te, st, halo_in, halo_out,
+                                 hp ? hp->pitch : 0, hp ? hp->stride : 0);
     if (r != cudaSuccess) return cuda_err(r, "fused RL iteration launch");
     ctx->launches += 1;
     return FDG_OK;
@@ -1151,7 +1162,21 @@ int solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long
     fdg_ctx* ctx = s->ctx;
     const long long stride = s->batch > 1 ? image_stride : (long long)pitch * s->H;
     const size_t n = (size_t)stride * s->batch;
-    CK(s->q.ensure(n));
+    // the fused engine iterates on two haloed u planes (replicated edge
+    // columns, so no CTA handles image edges in its pipeline); the two-pass
+    // engines use q
+    static const bool no_halo = getenv("FDG_FUSED_NOHALO") != nullptr;
+    const bool fused_h = use_fused(s->fwd.get()) && fused_halo_ok(s->W) && !no_halo;
+    HaloPlanes hp;
+    if (fused_h) {
+        hp.pitch = (s->W + fused_halo_left() + fused_halo_right() + 31) & ~31;
+        hp.stride = (long long)hp.pitch * s->H;
+        CK(s->uh.ensure(2 * (size_t)hp.stride * s->batch + 32));
+        hp.p[0] = s->uh.p + fused_halo_left();
+        hp.p[1] = hp.p[0] + (size_t)hp.stride * s->batch;
+    } else {
+        CK(s->q.ensure(n));
+    }
     cudaStream_t user = ctx->stream;
     // Replay the captured graph when the arguments and options are unchanged:
     // the whole run (start stamp + every iteration's launches) is one
@@ -1185,6 +1210,23 @@ int solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long
                               tr, st);
         CK(launch_stamp(tr.ts, st));
         ctx->launches += 1;
+        if (fused && fused_h) {
+            // iteration 0 reads f itself (u0 = f, replicated edges handled in
+            // the kernel), k = 1 .. n-2 ping-pong between the haloed planes,
+            // the last iteration writes d_u
+            for (int k = 0; k < iterations; ++k) {
+                const bool last = k == iterations - 1;
+                const float* src = k == 0 ? d_f : hp.p[(k - 1) & 1];
+                float* dst = last ? d_u : hp.p[k & 1];
+                const int slot = std::min(k, s->ntrace - 1);
+                int r = run_fused(ctx, s->fwd.get(), src, d_f, dst, pitch, s->W, s->H, s->batch, stride, &s->cfg,
+                                  tr.mc_at(slot), tr.nf_at(slot), tr.end_at(slot), st, 0, -1, 0, -1, &hp, k > 0,
+                                  !last);
+                if (r) return r;
+            }
+            if (iterations == 0) CK(cudaMemcpyAsync(d_u, d_f, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+            return FDG_OK;
+        }
         if (fused) {
             for (int k = 0; k < iterations; ++k) {
                 // ping-pong so the result lands in d_u; iteration 0 reads f itself (u0 = f)

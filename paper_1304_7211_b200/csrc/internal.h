@@ -141,9 +141,20 @@ void set_fused_mode(int v);
 int fused_mode();
 // Output rows [y0, y1), reads clamped into [ylo, yhi] (the image edges; rows
 // between a shard's core and those edges must hold valid halo rows).
+// halo_in / halo_out: u_in / u_out are haloed planes (pitch_h, bstride_h;
+// fused_halo_left() / _right() replicated columns around each row; the
+// pointer addresses column 0), else they use f's pitch and stride.  Halo
+// input needs W >= the kernel's strip width (fused_halo_ok).
 cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int y0, int y1, int ylo,
                          int yhi, int batch, long long bstride, float scale, float eps, int clamp,
-                         unsigned* maxchange, int* nanflag, unsigned long long* tend, cudaStream_t st);
+                         unsigned* maxchange, int* nanflag, unsigned long long* tend, cudaStream_t st,
+                         int halo_in = 0, int halo_out = 0, int pitch_h = 0, long long bstride_h = 0);
+int fused_halo_left();
+int fused_halo_right();
+bool fused_halo_ok(int W);
+// haloed copy of src (dst addresses column 0 of the haloed plane)
+cudaError_t launch_pad_halo(const float* src, int pitch_src, long long bs_src, float* dst, int pitch_dst,
+                            long long bs_dst, int W, int H, int batch, cudaStream_t st);
 // first non-finite / first negative row-major index (~0 if none) -> out[0..1]
 cudaError_t launch_validate(const float* f, int W, int H, int pitch, unsigned long long* out, cudaStream_t st);
 // one thread writes %globaltimer to *t (start stamp of a timed RL loop)

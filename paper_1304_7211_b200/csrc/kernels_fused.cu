@@ -34,7 +34,9 @@
 // segments with the barriers re-initialised in between -- so no CTA slot idles
 // (config 4: 34 strips x 8 bands would fill only 272 of 296 slots).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 #include <type_traits>
 
 #include "common.cuh"
@@ -43,6 +45,10 @@ namespace fdg {
 namespace {
 
 constexpr int REFRESH = 32;
+// haloed u planes (fused_halo_*): replicated columns left / right of each row,
+// enough for every strip's u segment [x0 - 16, x0 + 512) when W >= CW and
+// W % 4 == 0 (the last strip then ends exactly at W)
+constexpr int FUSED_HALO_L = 16, FUSED_HALO_R = 16;
 #ifndef FDG_QSLEEP
 #define FDG_QSLEEP 40
 #endif
@@ -64,7 +70,9 @@ struct FusedArgs {
     const float* u_in;
     const float* f;
     float* u_out;
-    int pitch, W, Wp4;
+    int pitch, W, Wp4;    // pitch: f's row pitch (elements)
+    int pitch_u, pitch_o;  // row pitches of u_in / u_out
+    long long bs_u, bs_o;  // image strides of u_in / u_out (batches)
     int y0, y1;    // output rows
     int ylo, yhi;  // readable rows; replicate clamping at these (image) edges
     int band, batch;
@@ -75,6 +83,9 @@ struct FusedArgs {
     unsigned* maxchange;
     int* nanflag;
     unsigned long long* tend;
+    unsigned long long* probe;  // diagnostics (FDG_FUSED_PROBE): per CTA {start, end, smid, rows}
+    int halo_in;   // u_in carries FUSED_HALO_L / _R replicated columns left / right of every row
+    int halo_out;  // write those columns of u_out too
 };
 
 // ---- packed fp32x2 arithmetic (Blackwell FADD2 / FMUL2 / FFMA2)
@@ -111,12 +122,6 @@ __device__ __forceinline__ float4 hsum15x4(const float* seg, int chunk) {
     return cat4(o01, o23);
 }
 
-// component k (0..3) of v, for the q columns outside the image that take the
-// clamped column's value
-__device__ __forceinline__ float pick(const float4 v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
-__device__ __forceinline__ float4 pick4(const float4 v, const int4 k) {
-    return make_float4(pick(v, k.x), pick(v, k.y), pick(v, k.z), pick(v, k.w));
-}
 
 // max that propagates NaN (the reference's clamp `value < 0 ? 0 : value`
 // keeps a NaN, and a NaN anywhere must reach the per-iteration check)
@@ -164,7 +169,10 @@ struct VRing {
     }
 };
 
-template <int RX, int RY, int NT, int R, int S, int QR>
+// PD: rows of u the B warps keep in flight (register prefetch depth);
+// HINT: u rows streamed with L2 evict_last (the B warps re-read them ~25 rows
+// later) and re-read with evict_first
+template <int RX, int RY, int NT, int R, int S, int QR, int PD, bool HINT>
 __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     using G = FG<RX, RY, NT>;
     static_assert(R == 2, "stage logic assumes two rows per stage");
@@ -185,8 +193,13 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     float4* v2 = v1 + MY * NT;                                    // MY x NT
 
     const int tid = threadIdx.x;
-    const long long img = (long long)blockIdx.z * a.bstride;
-    const long long pitch = a.pitch;
+#ifdef FDG_FUSED_PROBE
+    if (a.probe && tid == 0)  // diagnostics: start stamp parked in the barrier area's spare bytes
+        *reinterpret_cast<unsigned long long*>(smem_raw + 504) = globaltimer();
+#endif
+    const long long img = (long long)blockIdx.z * a.bstride;  // f
+    const long long img_u = (long long)blockIdx.z * a.bs_u, img_o = (long long)blockIdx.z * a.bs_o;
+    const long long pitch = a.pitch, pitch_u = a.pitch_u, pitch_o = a.pitch_o;
     // one column strip x0, output rows [yb0, yb1): fresh barriers, every role
     // runs its pipeline to the end of the segment
     auto run_segment = [&](const int x0, const int yb0, const int yb1) {
@@ -195,8 +208,16 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         const int j0 = qr_lo - RY;         // first streamed u row (may be < 0: clamped)
         const int steps = nq + 2 * RY;     // u rows streamed: j0 .. qr_hi + RY
         const int useg0 = x0 - 2 * G::HX;  // image column of u-segment index 0
-        // the u segment reaches outside the image: replicate columns 0 / W-1 there
-        const bool edge_cta = useg0 < 0 || x0 + G::CW + 2 * G::HX > a.W;
+        // the u segment reaches outside the image: replicate columns 0 / W-1
+        // there (not needed when u_in carries replicated halo columns)
+        const bool edge_cta = !a.halo_in && (useg0 < 0 || x0 + G::CW + 2 * G::HX > a.W);
+        const int lo_end = max(0, -useg0);       // segment indices [0, lo_end) are left of column 0
+        const int hi_beg = max(0, a.W - useg0);  // [hi_beg, UW) are right of column W-1
+#ifdef FDG_FUSED_NOEDGE
+        const bool prod_fix = false;  // diagnostics: timing without the edge-replication path (wrong edges)
+#else
+        const bool prod_fix = edge_cta;
+#endif
 
         if (tid == 0) {
             for (int s = 0; s < SS; ++s) {
@@ -215,11 +236,13 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         if (tid >= 2 * NT) {  // ------------------------------------ producer warp
             const int lane = tid - 2 * NT;
             const int nst = (steps + R - 1) / R;
-            const int uc0 = max(0, useg0), uc1 = min(a.Wp4, x0 + G::CW + 2 * G::HX);
+            const int uc0 = a.halo_in ? useg0 : max(0, useg0);
+            const int uc1 = a.halo_in ? useg0 + G::UW : min(a.Wp4, x0 + G::CW + 2 * G::HX);
             const unsigned ubytes = (unsigned)(uc1 - uc0) * 4u;
             const int udst = uc0 - useg0;
             const int fc0 = max(0, x0 - G::HX), fc1 = min(a.Wp4, x0 + G::CW + G::HX);
             const unsigned fbytes = (unsigned)(fc1 - fc0) * 4u;
+            const uint64_t pol_last = HINT ? policy_evict_last() : 0;
             auto issue = [&](int st) {
                 const int s = st % SS;
                 if (st >= SS) mbar_wait_sleep(&empty[s], ((st / SS) - 1) & 1, 200);
@@ -227,19 +250,23 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
                 mbar_arrive_expect_tx(&full[s], ubytes * nr);
                 for (int r = 0; r < nr; ++r) {
                     const int j = j0 + st * R + r;
-                    bulk_g2s(uring + (size_t)(s * R + r) * G::USEG + udst,
-                             a.u_in + img + (long long)clampi(j, a.ylo, a.yhi) * pitch + uc0, ubytes, &full[s]);
+                    if (HINT)
+                        bulk_g2s_hint(uring + (size_t)(s * R + r) * G::USEG + udst,
+                                      a.u_in + img_u + (long long)clampi(j, a.ylo, a.yhi) * pitch_u + uc0, ubytes,
+                                      &full[s], pol_last);
+                    else
+                        bulk_g2s(uring + (size_t)(s * R + r) * G::USEG + udst,
+                                 a.u_in + img_u + (long long)clampi(j, a.ylo, a.yhi) * pitch_u + uc0, ubytes,
+                                 &full[s]);
                     if (j - RY >= qr_lo && j - RY <= qr_hi)
                         l2_prefetch(a.f + img + (long long)(j - RY) * pitch + fc0, fbytes);
                 }
             };
-            if (!edge_cta) {
+            if (!prod_fix) {
                 if (lane == 0)
                     for (int st = 0; st < nst; ++st) issue(st);
                 return;
             }
-            const int lo_end = max(0, -useg0);       // segment indices [0, lo_end) are left of column 0
-            const int hi_beg = max(0, a.W - useg0);  // [hi_beg, UW) are right of column W-1
             const int i0c = lo_end, iWc = a.W - 1 - useg0;
             for (int st = 0; st < nst + LAG; ++st) {
                 if (st < nst && lane == 0) issue(st);
@@ -267,18 +294,61 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         const float scale = a.scale, eps = a.eps;
 
         if (tid < NT) {  // ---------------------------------- A warps: q rows
-            uint64_t* gate = edge_cta ? ready : full;
+            uint64_t* gate = prod_fix ? ready : full;
             const int qc = x0 - G::HX + 4 * tid;  // first q column of this thread
-            // q columns outside the image take the clamped column's value: such a
-            // thread computes the 4-column group qcl holding the clamped columns
-            // and picks components (warp-uniform)
-            const int wq0 = x0 - G::HX + 128 * (tid >> 5);
-            const bool edgeA = wq0 < 0 || wq0 + 127 > a.W - 1;
-            const int qcl = min(max(qc, 0), (a.W - 1) & ~3);
-            const int4 sel = make_int4(clampi(qc, 0, a.W - 1) - qcl, clampi(qc + 1, 0, a.W - 1) - qcl,
-                                       clampi(qc + 2, 0, a.W - 1) - qcl, clampi(qc + 3, 0, a.W - 1) - qcl);
-            const int chunk = (qcl - qc) / 4 + tid;
-            const float* fcol = a.f + img + qcl;
+            // q columns outside the image take the edge column's value (q is
+            // replicate-continued for the adjoint pass): the thread owning
+            // column 0 / W-1 writes those slots of the q row itself, threads
+            // wholly outside the image compute throwaway values and store
+            // nothing (the edge stays out of the hot path's arithmetic: a
+            // per-row component select in the edge warp gated the whole
+            // CTA's pipeline -- edge strips ran ~40 % slower)
+            const int c0 = x0 - G::HX;  // image column of q-row index 0
+            const bool outside = qc + 3 < 0 || qc > a.W - 1;
+            // owner of column W-1 when the q row reaches past it (also makes its
+            // own components beyond W-1 take that column's value)
+            const bool ownR = qc <= a.W - 1 && a.W - 1 <= qc + 3 && (c0 + G::QW > a.W || qc + 3 > a.W - 1);
+            const int tR = (a.W - 1 - c0) >> 2;  // A thread owning column W-1 (if in this strip)
+            // edge warps: the threads left of column 0 take q(0) from lane 2 (the
+            // owner of column 0, x0 == 0), those right of W-1 take q(W-1) from its
+            // owner -- one shuffle each when the owner shares their warp (it does
+            // unless the image is narrower than ~400 columns: then the owner
+            // fills those slots with scalar stores)
+            const int wid = tid >> 5;
+            const bool wL = c0 < 0 && wid == 0;
+            const bool rInStrip = tR >= 0 && tR < NT && c0 + G::QW > a.W;
+            const bool wR = rInStrip && wid == NT / 32 - 1 && (tR >> 5) == wid;
+            const bool slowR = ownR && !((tR >> 5) == NT / 32 - 1);
+            const bool edgeW = wL || wR || (rInStrip && wid == (tR >> 5)) || outside;
+            const int chunk = tid;
+            const float* fcol = a.f + img + clampi(qc, 0, a.Wp4 - 4);
+            // store of this thread's q chunk into q row buffer `qrow`
+            auto put_q = [&](float* qrow, float4 q) {
+                if (!edgeW) {  // warp-uniform for interior warps
+                    *reinterpret_cast<float4*>(qrow + 4 * tid) = q;
+                    return;
+                }
+                float vR = q.w;
+                if (ownR) {
+                    const int e = a.W - 1 - qc;
+                    vR = e == 0 ? q.x : e == 1 ? q.y : e == 2 ? q.z : q.w;
+                    if (e < 3) q.w = vR;
+                    if (e < 2) q.z = vR;
+                    if (e < 1) q.y = vR;
+                }
+                if (wL) {
+                    const float qL = __shfl_sync(0xffffffffu, q.x, 2);
+                    if (qc + 3 < 0) q = make_float4(qL, qL, qL, qL);
+                }
+                if (wR) {
+                    const float qR = __shfl_sync(0xffffffffu, vR, tR & 31);
+                    if (qc > a.W - 1) q = make_float4(qR, qR, qR, qR);
+                }
+                if (outside && !wL && !wR) return;  // filled by the owner (slowR)
+                *reinterpret_cast<float4*>(qrow + 4 * tid) = q;
+                if (slowR)
+                    for (int c = qc + 4; c < c0 + G::QW; ++c) qrow[c - c0] = vR;
+            };
             VRing<MY> r1;
             int s = 0;
             unsigned phase = 0;
@@ -318,18 +388,16 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
                         phase ^= 1u;
                     }
                 }
-                if (edgeA) h = pick4(h, sel);
                 if (ST)
                     r1.push_full(v1, NT, tid, h);
                 else
                     r1.push(v1, NT, tid, h);
                 const int r = i - 2 * RY;
                 if (ST || r >= 0) {
-                    const float4 fv = edgeA ? pick4(fx, sel) : fx;
                     // f / max(v, eps): max.NaN keeps the reference's NaN propagation
-                    const float4 q = quot4(r1.col, fv);
+                    const float4 q = quot4(r1.col, fx);
                     if (ST || r >= QR) mbar_wait(&qempty[r & (QR - 1)], ((r / QR) - 1) & 1);
-                    *reinterpret_cast<float4*>(qrow_ptr(r) + 4 * tid) = q;
+                    put_q(qrow_ptr(r), q);
                     mbar_arrive(&qfull[r & (QR - 1)]);
                 }
                 if (!ST) fx = load_f(i + 2);
@@ -365,21 +433,17 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
                             s = 0;
                             phase ^= 1u;
                         }
-                        if (edgeA) {
-                            h0 = pick4(h0, sel);
-                            h1 = pick4(h1, sel);
-                        }
                         r1.push_full(v1, NT, tid, h0);
-                        const float4 qa = quot4(r1.col, edgeA ? pick4(F0, sel) : F0);
+                        const float4 qa = quot4(r1.col, F0);
                         r1.push_full(v1, NT, tid, h1);
-                        const float4 qb = quot4(r1.col, edgeA ? pick4(F1, sel) : F1);
+                        const float4 qb = quot4(r1.col, F1);
                         F0 = ldg4(fp);
                         F1 = ldg4(fp + pitch);
                         const int r = i - 2 * RY;  // even: slots r, r + 1 in the same ring turn
                         mbar_wait(&qempty[r & (QR - 1)], ((r / QR) - 1) & 1);
                         mbar_wait(&qempty[(r + 1) & (QR - 1)], (((r + 1) / QR) - 1) & 1);
-                        *reinterpret_cast<float4*>(qrow_ptr(r) + 4 * tid) = qa;
-                        *reinterpret_cast<float4*>(qrow_ptr(r + 1) + 4 * tid) = qb;
+                        put_q(qrow_ptr(r), qa);
+                        put_q(qrow_ptr(r + 1), qb);
                         mbar_arrive(&qfull[r & (QR - 1)]);
                         mbar_arrive(&qfull[(r + 1) & (QR - 1)]);
     #endif
@@ -402,13 +466,27 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         const int oc = x0 + 4 * tb;
         const bool has_out = tb < G::NB && oc < a.W;  // lanes past the strip compute, never store
         const bool full_store = oc + 3 < a.W;
+        // replicated halo columns of u_out: the owners of columns 0 / W-1
+        // replicated halo columns of u_out (halo mode needs W % 4 == 0): B warp 0
+        // of the x0 = 0 strip writes columns -16..-1 from lanes 1..4, the warp
+        // holding column W-1 writes W..W+15 from the lanes past the image
+        // (values shuffled from the edge owners; one store per lane)
+        const int bw = tid >> 5;
+        const bool bL = a.halo_out && x0 == 0 && bw == (NT >> 5);
+        const int tbR = (a.W - 4 - x0) >> 2;  // B thread holding columns W-4..W-1
+        const bool bR = a.halo_out && tbR >= 0 && tbR + 4 < NT && ((NT + tbR) >> 5) == bw &&
+                        ((NT + tbR + 4) >> 5) == bw;
         const int ocl = min(oc, a.Wp4 - 4);
-        const float* ucol = a.u_in + img + ocl;
-        float* ocol = a.u_out + img + oc;
+        const float* ucol = a.u_in + img_u + ocl;
+        float* ocol = a.u_out + img_o + oc;
         VRing<MY> r2;
         float4 hlast = make_float4(0.f, 0.f, 0.f, 0.f);
         float maxd = 0.f;
-        auto load_u = [&](int o) { return ldg4(ucol + min(yb0 + o, yb1 - 1) * pitch); };  // u of output o
+        const uint64_t pol_first = HINT ? policy_evict_first() : 0;
+        auto load_u = [&](int o) {  // u of output o
+            const float* p = ucol + min(yb0 + o, yb1 - 1) * pitch_u;
+            return HINT ? ldg4_hint(p, pol_first) : ldg4(p);
+        };
         auto store = [&](auto fs, const int o, const float4 c, const float4 u) {
             constexpr bool FS = decltype(fs)::value;
             const bool fst = FS || full_store;
@@ -421,8 +499,21 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
             const float dd[4] = {dv.x, dv.y, dv.z, dv.w};
     #pragma unroll
             for (int e = 0; e < 4; ++e)
-                if (fst || oc + e < a.W) maxd = fmax_nan(maxd, fabsf(dd[e]));
-            float* outp = ocol + (yb0 + o) * pitch;
+                if (has_out && (fst || oc + e < a.W)) maxd = fmax_nan(maxd, fabsf(dd[e]));
+            float* outp = ocol + (yb0 + o) * pitch_o;
+            if (bL | bR) {  // warp-uniform: edge warps only
+                if (bL) {
+                    const float v0 = __shfl_sync(0xffffffffu, val[0], 0);
+                    if (tb >= 1 && tb <= FUSED_HALO_L / 4)
+                        *reinterpret_cast<float4*>(outp - oc - 4 * tb) = make_float4(v0, v0, v0, v0);
+                }
+                if (bR) {
+                    const float vR = __shfl_sync(0xffffffffu, val[3], (NT + tbR) & 31);
+                    if (oc >= a.W && oc < a.W + FUSED_HALO_R)
+                        *reinterpret_cast<float4*>(outp) = make_float4(vR, vR, vR, vR);
+                }
+            }
+            if (!has_out) return;
             if (fst) {
                 *reinterpret_cast<float4*>(outp) = make_float4(val[0], val[1], val[2], val[3]);
             } else {
@@ -443,7 +534,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         const int band = yb1 - yb0;
         auto push_out = [&](const float4 h, float4 u) {
             r2.push(v2, NT, tb, h);
-            if (r2.n >= MY && has_out) store(std::false_type(), r2.n - MY, r2.col, u);
+            if (r2.n >= MY) store(std::false_type(), r2.n - MY, r2.col, u);
         };
         // warm-up: q rows 0 .. r_s-1 (ring not yet full)
         const int r_s = (max(1, 2 * RY + 1 - extras) + 1) & ~1;
@@ -461,6 +552,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
             // here r2 is full and output o = r + extras - 2 RY follows every push
             const int o0 = r + extras - 2 * RY;
             float4 U0 = load_u(o0), U1 = load_u(o0 + 1);
+            float4 U2 = PD > 2 ? load_u(o0 + 2) : U0, U3 = PD > 2 ? load_u(o0 + 3) : U1;
             auto blocks = [&](auto fs) {
                 for (int b = 0; b < nblk; ++b) {
     #pragma unroll 1
@@ -469,11 +561,18 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
                         const float4 g0 = take(r);
                         const float4 g1 = take(r + 1);
                         r2.push_full(v2, NT, tb, g0);
-                        if (has_out) store(fs, o, r2.col, U0);
+                        store(fs, o, r2.col, U0);
                         r2.push_full(v2, NT, tb, g1);
-                        if (has_out) store(fs, o + 1, r2.col, U1);
-                        U0 = load_u(o + 2);
-                        U1 = load_u(o + 3);
+                        store(fs, o + 1, r2.col, U1);
+                        if (PD > 2) {
+                            U0 = U2;
+                            U1 = U3;
+                            U2 = load_u(o + 4);
+                            U3 = load_u(o + 5);
+                        } else {
+                            U0 = load_u(o + 2);
+                            U1 = load_u(o + 3);
+                        }
                         hlast = g1;
                     }
                     r2.refresh(v2, NT, tb);  // fp32 drift
@@ -529,26 +628,59 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         const int sx = (int)(p / rows), r0 = (int)(p - (long long)sx * rows);
         const int r1 = (int)min((long long)rows, r0 + (end - p));
         if (!first) reset_barriers();
-        run_segment(sx * G::CW, a.y0 + r0, a.y0 + r1);
+        // the last strip is shifted left to end at the image edge (overlapping
+        // its neighbour, whose columns it rewrites with identical values): a
+        // strip reaching far past column W-1 makes the producer replicate
+        // hundreds of columns per row and straggles the whole launch
+        const int xs = a.W > G::CW ? min(sx * G::CW, (a.W - G::CW + 3) & ~3) : 0;
+        run_segment(xs, a.y0 + r0, a.y0 + r1);
         p += r1 - r0;
     }
+#ifdef FDG_FUSED_PROBE
+    if (a.probe) {
+        __syncthreads();
+        if (tid == 0) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            unsigned long long* q = a.probe + 4 * (size_t)blockIdx.x;
+            q[0] = *reinterpret_cast<const unsigned long long*>(smem_raw + 504);
+            q[1] = globaltimer();
+            q[2] = smid;
+            q[3] = (unsigned long long)(end - (a.lin_len > 0 ? (long long)blockIdx.x * a.lin_len : 0));
+        }
+    }
+#endif
 }
 
-template <int RX, int RY, int NT, int R, int S, int QR>
+// dst row y = src row y with FUSED_HALO_L / _R replicated columns (dst
+// points at column 0 of a haloed plane)
+__global__ void k_pad_halo(const float* __restrict__ src, int pitch_src, long long bs_src, float* __restrict__ dst,
+                           int pitch_dst, long long bs_dst, int W, int H) {
+    const int y = blockIdx.y;
+    const long long b = blockIdx.z;
+    const float* sr = src + b * bs_src + (long long)y * pitch_src;
+    float* dr = dst + b * bs_dst + (long long)y * pitch_dst;
+    for (int x = (int)threadIdx.x + blockIdx.x * blockDim.x - FUSED_HALO_L; x < W + FUSED_HALO_R;
+         x += blockDim.x * gridDim.x)
+        dr[x] = sr[min(max(x, 0), W - 1)];
+}
+
+template <int RX, int RY, int NT, int R, int S, int QR, int PD, bool HINT>
 size_t smem_bytes() {
     using G = FG<RX, RY, NT>;
     return 512 + sizeof(float) * ((size_t)S * G::USEG + QR * (size_t)G::QSEG) + sizeof(float4) * 2 * (size_t)G::MY * NT;
 }
 
-template <int RX, int RY, int NT, int R, int S, int QR>
+template <int RX, int RY, int NT, int R, int S, int QR, int PD, bool HINT>
 cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     using G = FG<RX, RY, NT>;
-    const size_t smem = smem_bytes<RX, RY, NT, R, S, QR>();
-    cudaError_t err = smem_attr<k_fused<RX, RY, NT, R, S, QR>>();
+    const size_t smem = smem_bytes<RX, RY, NT, R, S, QR, PD, HINT>();
+    cudaError_t err = smem_attr<k_fused<RX, RY, NT, R, S, QR, PD, HINT>>();
     if (err != cudaSuccess) return err;
     static int occ = 0;
     if (!occ) {
-        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused<RX, RY, NT, R, S, QR>, 2 * NT + 32, smem);
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused<RX, RY, NT, R, S, QR, PD, HINT>, 2 * NT + 32,
+                                                            smem);
         if (err != cudaSuccess) return err;
         if (occ < 1) occ = 1;
     }
@@ -583,8 +715,31 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
             grid = dim3((unsigned)((total + L - 1) / L), 1, 1);
         }
     }
-    k_fused<RX, RY, NT, R, S, QR><<<grid, 2 * NT + 32, smem, st>>>(a);
-    return cudaGetLastError();
+#ifdef FDG_FUSED_PROBE
+    static const char* probe_path = getenv("FDG_FUSED_PROBE");
+#else
+    static const char* probe_path = nullptr;
+#endif
+    static unsigned long long* d_probe = nullptr;
+    a.probe = nullptr;
+    if (probe_path) {
+        if (!d_probe) cudaMalloc(&d_probe, 4 * sizeof(unsigned long long) * 65536);
+        a.probe = d_probe;
+    }
+    k_fused<RX, RY, NT, R, S, QR, PD, HINT><<<grid, 2 * NT + 32, smem, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (probe_path && e == cudaSuccess) {  // diagnostics only (eager launches): append the per-CTA record
+        const size_t n = (size_t)grid.x * grid.y * grid.z;
+        std::vector<unsigned long long> h(4 * n);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h.data(), d_probe, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+        if (FILE* fp = fopen(probe_path, "a")) {
+            for (size_t i = 0; i < n; ++i) fprintf(fp, "%zu %llu %llu %llu %llu\n", i, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+            fprintf(fp, "--\n");
+            fclose(fp);
+        }
+    }
+    return e;
 }
 
 // Engine selection: 1 = on (default; beats the two-pass engine on config 4),
@@ -600,10 +755,29 @@ bool fused_supported(int mx, int my, int min_dx, int min_dy) {
     return g_fused.load() == 1 && mx == 15 && my == 15 && min_dx == -7 && min_dy == -7;
 }
 
+int fused_halo_left() { return FUSED_HALO_L; }
+int fused_halo_right() { return FUSED_HALO_R; }
+bool fused_halo_ok(int W) { return W >= FG<7, 7, 128>::CW && W % 4 == 0; }
+
+cudaError_t launch_pad_halo(const float* src, int pitch_src, long long bs_src, float* dst, int pitch_dst,
+                            long long bs_dst, int W, int H, int batch, cudaStream_t st) {
+    const int threads = 256;
+    const int bx = std::max(1, std::min(8, (W + FUSED_HALO_L + FUSED_HALO_R + threads - 1) / threads));
+    k_pad_halo<<<dim3(bx, H, batch), threads, 0, st>>>(src, pitch_src, bs_src, dst, pitch_dst, bs_dst, W, H);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int y0, int y1, int ylo,
                          int yhi, int batch, long long bstride, float scale, float eps, int clamp, unsigned* maxchange, int* nanflag,
-                         unsigned long long* tend, cudaStream_t st) {
+                         unsigned long long* tend, cudaStream_t st, int halo_in, int halo_out, int pitch_h,
+                         long long bstride_h) {
     FusedArgs a;
+    a.halo_in = halo_in;
+    a.halo_out = halo_out;
+    a.pitch_u = halo_in ? pitch_h : pitch;  // haloed planes share one pitch
+    a.pitch_o = halo_out ? pitch_h : pitch;
+    a.bs_u = halo_in ? bstride_h : bstride;
+    a.bs_o = halo_out ? bstride_h : bstride;
     a.u_in = u_in;
     a.f = f;
     a.u_out = u_out;
@@ -624,9 +798,10 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
     a.tend = tend;
     static const int variant = getenv("FDG_FUSED_V") ? atoi(getenv("FDG_FUSED_V")) : 0;
     switch (variant) {
-        case 1: return launch_t<7, 7, 128, 2, 8, 16>(a, st);
-        case 2: return launch_t<7, 7, 128, 2, 16, 8>(a, st);
-        default: return launch_t<7, 7, 128, 2, 12, 8>(a, st);
+        case 1: return launch_t<7, 7, 128, 2, 12, 8, 4, false>(a, st);
+        case 2: return launch_t<7, 7, 128, 2, 12, 8, 2, true>(a, st);
+        case 3: return launch_t<7, 7, 128, 2, 12, 8, 4, true>(a, st);
+        default: return launch_t<7, 7, 128, 2, 12, 8, 2, false>(a, st);
     }
 }
 
