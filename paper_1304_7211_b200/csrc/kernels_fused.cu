@@ -798,10 +798,8 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
     a.tend = tend;
     static const int variant = getenv("FDG_FUSED_V") ? atoi(getenv("FDG_FUSED_V")) : 0;
     switch (variant) {
-        case 1: return launch_t<7, 7, 128, 2, 12, 8, 4, false>(a, st);
-        case 2: return launch_t<7, 7, 128, 2, 12, 8, 2, true>(a, st);
-        case 3: return launch_t<7, 7, 128, 2, 12, 8, 4, true>(a, st);
-        default: return launch_t<7, 7, 128, 2, 12, 8, 2, false>(a, st);
+        case 1: return launch_t<7, 7, 128, 2, 12, 8, 2, false>(a, st);  // no L2 cache hints
+        default: return launch_t<7, 7, 128, 2, 12, 8, 2, true>(a, st);
     }
 }
 
