@@ -502,7 +502,7 @@ def run_thinned(args, cfg, world, rank, local):
                               "thinned config 3 is a single-image replica (SURVEY 8e)"}))
         return 0
     torch.cuda.set_device(local)
-    thr = json.load(open(os.path.join(ROOT, "profiles", "r01_cfg3_thresholds.json")))[args.thin]["threshold"]
+    thr = W.CFG3_THRESHOLDS[args.thin]
     iters = args.iterations or cfg.iterations
     psf = W.make_psf(cfg.psf)
     _, f = W.make_input(cfg)

@@ -1,0 +1,164 @@
+"""Full-size parity of every BASELINE configuration against the CPU oracle,
+in the driver-run GPU suite (VERDICT r1 "next" #1).
+
+The oracle (oracle/liboracle.so, bit-identical to the reference compiled
+from its own headers, tests/test_oracle.py) runs on the host's cores in ONE
+background worker thread that starts when the first test of this module
+asks for it; the ctypes calls release the GIL, so the GPU runs of earlier
+configs overlap the oracle runs of later ones.  Wall time on the B200 box
+(16 host threads): ~5 min, dominated by the three 4096^2 dense runs.
+
+Bar: max |u_gpu - u_ref| / |u_ref| <= 1e-4 after the configured
+iteration count and |PSNR(u_gpu, g) - PSNR(u_ref, g)| <= 0.01 dB (peak 1);
+thinned config 3: the per-iteration active masks replayed from the oracle,
+inactive fractions equal, active lists and (y, x0, len) runs bit-exact
+(convolve.hpp:450-465).
+"""
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+from paper_1304_7211_b200 import OperatorKind as K, RlConfig, RlSolver, rlDeconvolve, rlDeconvolveSelective
+from paper_1304_7211_b200 import workloads as W
+from paper_1304_7211_b200.convolve import maskRuns
+
+pytestmark = pytest.mark.gpu
+MAX_REL = 1e-4
+DPSNR = 0.01
+OPS = {"box1d-sliding": K.Box1dSliding, "box2d-sliding": K.Box2dSliding, "generic-box": K.GenericBox,
+       "naive": K.Naive}
+CFG4B_CHECKED = tuple(range(0, 64, 8))  # 8 of the 64 batch images
+
+
+def _plain(name):
+    cfg = W.CONFIGS[name]
+    g, f = W.make_input(cfg)
+    psf = W.make_psf(cfg.psf)
+    ref, mc, _ = O.rl_deconvolve(f.astype(np.float64), psf, cfg.iterations, int(OPS[cfg.op]))
+    return {"g": g, "f": f, "psf": psf, "ref": ref, "mc": mc}
+
+
+def _thinned(label):
+    cfg = W.CONFIGS["cfg3"]
+    g, f = W.make_input(cfg)
+    psf = W.make_psf(cfg.psf)
+    thr = W.CFG3_THRESHOLDS[label]
+    ref, inact, _, masks = O.rl_selective(f.astype(np.float64), psf, cfg.iterations, thr, W.CFG3_PERIOD,
+                                          W.CFG3_THIN_START, O.NAIVE, record_masks=True)
+    return {"g": g, "f": f, "psf": psf, "ref": ref, "inact": inact, "masks": masks, "thr": thr}
+
+
+def _batch():
+    cfg = W.CONFIGS["cfg4b"]
+    psf = W.make_psf(cfg.psf)
+    imgs = [W.make_input(cfg, image=i) for i in range(cfg.batch)]
+    refs = {i: O.rl_deconvolve(imgs[i][1].astype(np.float64), psf, cfg.iterations, O.BOX1D_SLIDING)[0]
+            for i in CFG4B_CHECKED}
+    return {"imgs": imgs, "psf": psf, "refs": refs}
+
+
+class _OracleQueue:
+    """One worker, jobs in test order; each job = inputs + oracle result."""
+
+    def __init__(self):
+        self.ex = ThreadPoolExecutor(max_workers=1)
+        self.fut = {}
+        self.lock = threading.Lock()
+        for key, fn in (("cfg2", lambda: _plain("cfg2")), ("cfg4b", _batch), ("cfg4", lambda: _plain("cfg4")),
+                        ("cfg3", lambda: _plain("cfg3")), ("active50", lambda: _thinned("active50")),
+                        ("active25", lambda: _thinned("active25"))):
+            self.fut[key] = self.ex.submit(fn)
+
+    def take(self, key):
+        with self.lock:
+            fut = self.fut.pop(key)  # released after use (the 4096^2 mask stacks are 2.5 GB each)
+        return fut.result()
+
+
+@pytest.fixture(scope="module")
+def oq():
+    q = _OracleQueue()
+    yield q
+    q.ex.shutdown(wait=False, cancel_futures=True)
+
+
+def _check(name, u, ref, g):
+    err = W.max_rel(u, ref)
+    dp = abs(W.psnr(u, g) - W.psnr(ref, g))
+    assert err <= MAX_REL, f"{name}: max-rel {err:.3e}"
+    assert dp <= DPSNR, f"{name}: dPSNR {dp:.5f} dB"
+    return err, dp
+
+
+def _plain_case(oq, name):
+    d = oq.take(name)
+    cfg = W.CONFIGS[name]
+    res = rlDeconvolve(d["f"], d["psf"], RlConfig(iterations=cfg.iterations, op=OPS[cfg.op]))
+    _check(name, res.image, d["ref"], d["g"])
+    gm = np.array([r.maxAbsChange for r in res.trace.records])
+    np.testing.assert_allclose(gm, d["mc"], rtol=2e-2, atol=1e-6)
+
+
+def test_cfg2_full_2048_200it(oq):
+    _plain_case(oq, "cfg2")
+
+
+def test_cfg4b_batch64_one_launch(oq):
+    """The benchmarked cfg4b path: ONE RlSolver(batch=64) run over all 64
+    images (row-resident engine, batch over blockIdx.z), 8 checked."""
+    torch = pytest.importorskip("torch")
+    d = oq.take("cfg4b")
+    cfg = W.CONFIGS["cfg4b"]
+    solver = RlSolver(d["psf"], RlConfig(iterations=cfg.iterations, op=K.Box1dSliding), cfg.width, cfg.height,
+                      batch=cfg.batch)
+    assert solver.engine() == "rowres"
+    f = torch.from_numpy(np.stack([x[1] for x in d["imgs"]])).cuda()
+    u = torch.empty_like(f)
+    before = solver.launches()
+    solver.run(f, u)
+    torch.cuda.synchronize()
+    assert solver.launches() - before >= 1
+    out = u.cpu().numpy()
+    for i in CFG4B_CHECKED:
+        _check(f"cfg4b[{i}]", out[i], d["refs"][i], d["imgs"][i][0])
+
+
+def test_cfg4_full_16384_fused(oq):
+    """16384^2 x 100 through the default (fused, work-balanced) engine."""
+    d = oq.take("cfg4")
+    cfg = W.CONFIGS["cfg4"]
+    solver = RlSolver(d["psf"], RlConfig(iterations=cfg.iterations, op=K.Box2dSliding), cfg.width, cfg.height)
+    assert solver.engine() == "fused"
+    del solver
+    res = rlDeconvolve(d["f"], d["psf"], RlConfig(iterations=cfg.iterations, op=K.Box2dSliding))
+    _check("cfg4", res.image, d["ref"], d["g"])
+    gm = np.array([r.maxAbsChange for r in res.trace.records])
+    np.testing.assert_allclose(gm, d["mc"], rtol=2e-2, atol=1e-6)
+
+
+def test_cfg3_full_4096_unthinned(oq):
+    _plain_case(oq, "cfg3")
+
+
+@pytest.mark.parametrize("label", ["active50", "active25"])
+def test_cfg3_full_thinned_mask_replay(oq, label):
+    d = oq.take(label)
+    cfg = W.CONFIGS["cfg3"]
+    masks = d["masks"]
+    res = rlDeconvolveSelective(d["f"], d["psf"], RlConfig(iterations=cfg.iterations, op=K.Naive), d["thr"],
+                                W.CFG3_PERIOD, thin_start=W.CFG3_THIN_START, mask_replay=masks,
+                                record_masks=True)
+    assert np.array_equal(res.masks, masks)
+    inact = np.array([r.inactiveFraction for r in res.trace.records])
+    assert np.array_equal(inact, d["inact"])
+    act = 1 - d["inact"][W.CFG3_THIN_START:].mean()
+    want = {"active50": 0.50, "active25": 0.25}[label]
+    assert abs(act - want) < 0.02, f"{label}: mean active fraction {act:.3f}"
+    for k in (W.CFG3_THIN_START, W.CFG3_THIN_START + 1, 75, cfg.iterations - 1):
+        idx, runs = maskRuns(masks[k])
+        assert np.array_equal(idx, O.active_list(masks[k]))
+        assert np.array_equal(runs, O.mask_runs(masks[k]))
+    _check(f"cfg3-{label}", res.image, d["ref"], d["g"])
