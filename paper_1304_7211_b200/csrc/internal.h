@@ -108,7 +108,14 @@ cudaError_t launch_dense(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
                          const int* d_tile_blocks, const int* d_tile_count);
 cudaError_t launch_spans(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st);
 bool spans_supported(const DevPsf& p);
-// spans kernel choice: 0 = by image size (tile <= 4.5 Mpx per launch), 1 = tile, 2 = marching
+// runtime span-table kernel (kernels_spanr.cu): any row-convex PSF with
+// <= 64 rows and max_dx - min_dx <= 64
+bool spanr_supported(const DevPsf& p);
+cudaError_t launch_spanr(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st);
+// "tile" / "marching" (compile-time tables) or "runtime-table"
+const char* spans_kernel(const DevPsf& p, long long px);
+// spans kernel choice: 0 = by image size (tile <= 4.5 Mpx per launch), 1 = tile, 2 = marching,
+// 3 = the runtime-table kernel for every shape
 void set_spans_mode(int v);
 int spans_mode();
 bool dense_supported(const DevPsf& p);

@@ -1,8 +1,9 @@
 // kernels_spans.cu -- "spans" engine: row-convex uniform PSFs (GenericBox,
 // convolve.hpp:177-212) whose span table is known at compile time -- the
 // BASELINE disc r<=10 (config 2, 21 rows, 317 taps) and the 21 px @ 30 deg
-// oblique line (config 1, 11 rows, 29 taps).  Other row-convex PSFs use the
-// generic "taps" engine.
+// oblique line (config 1, 11 rows, 29 taps).
+//
+// Any other row-convex PSF runs the runtime-table kernel (kernels_spanr.cu).
 //
 // Two kernels (choice by image size in launch_shape):
 //
@@ -661,13 +662,25 @@ int spans_mode() { return g_spans_mode.load(); }
 
 bool spans_supported(const DevPsf& p) {
     if (getenv("FDG_NO_SPANS")) return false;
-    return same_shape<DiscR10>(p) || same_shape<Oblique21>(p);
+    return same_shape<DiscR10>(p) || same_shape<Oblique21>(p) || spanr_supported(p);
 }
 
+// compile-time tables first (unless spans mode 3 forces the runtime-table
+// kernel, for A/B and tests), then the runtime-table kernel (kernels_spanr.cu)
 cudaError_t launch_spans(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st) {
-    if (same_shape<DiscR10>(p)) return launch_shape<DiscR10>(p, g, e, st);
-    if (same_shape<Oblique21>(p)) return launch_shape<Oblique21>(p, g, e, st);
-    return cudaErrorNotSupported;
+    if (spans_mode() != 3) {
+        if (same_shape<DiscR10>(p)) return launch_shape<DiscR10>(p, g, e, st);
+        if (same_shape<Oblique21>(p)) return launch_shape<Oblique21>(p, g, e, st);
+    }
+    return launch_spanr(p, g, e, st);
+}
+
+const char* spans_kernel(const DevPsf& p, long long px) {
+    if (spans_mode() != 3 && (same_shape<DiscR10>(p) || same_shape<Oblique21>(p))) {
+        const int mode = spans_mode();
+        return (mode ? mode == 1 : px <= 4608ll * 1024) ? "tile" : "marching";
+    }
+    return "runtime-table";
 }
 
 }  // namespace fdg

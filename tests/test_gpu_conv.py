@@ -14,8 +14,8 @@ from oracle import pyoracle as O
 from paper_1304_7211_b200 import (ConvCounters, ConvPlan, OperatorKind as K, convolve, maskedConvolve,
                                   workloads as W)
 from paper_1304_7211_b200.convolve import (box1dCumulatedConvolve, box1dSlidingConvolve, maskRuns)
-from paper_1304_7211_b200.psf import (DensePsf, SparsePsf, makeBoxPsf, makeDiagonalPsf, makeDiscPsf,
-                                      makeLinePsf)
+from paper_1304_7211_b200.psf import (DensePsf, SparsePsf, UniformConvexPsf, makeBoxPsf, makeDiagonalPsf,
+                                      makeDiscPsf, makeLinePsf)
 
 pytestmark = pytest.mark.gpu
 REL = 2e-6
@@ -136,7 +136,9 @@ def test_engine_selection():
     assert ConvPlan(makeDiagonalPsf(9), K.List).engine() == "taps"
     assert ConvPlan(W.disc_r10(), K.GenericBox).engine() == "spans"
     assert ConvPlan(W.oblique_line(), K.GenericBox).engine() == "spans"
-    assert ConvPlan(makeDiscPsf(9), K.GenericBox).engine() == "taps"
+    assert ConvPlan(makeDiscPsf(9), K.GenericBox).engine() == "spans"  # runtime span table
+    assert ConvPlan(convex_zoo()["wide65"], K.GenericBox).engine() == "taps"  # x extent 65 > 64
+    assert ConvPlan(convex_zoo()["tall65"], K.GenericBox).engine() == "taps"  # 65 rows > 64
 
 
 @pytest.mark.parametrize("mode", [1, 2])
@@ -156,3 +158,80 @@ def test_spans_kernels_both_paths(mode, name):
             close(convolve(img, psf, K.GenericBox), O.convolve(img, psf, O.GENERIC_BOX))
     finally:
         lib().fdg_set_option(b"spans", prev)
+
+
+def _oblique(length, angle_deg):
+    """Row-convex rasterised line through the origin (the cfg1 rasteriser at
+    another angle): UniformConvexPsf rows."""
+    import math
+    pts = set()
+    t = -length / 2.0
+    while t <= length / 2.0 + 1e-12:
+        x = math.floor(t * math.cos(math.radians(angle_deg)) + 0.5)
+        y = -math.floor(t * math.sin(math.radians(angle_deg)) + 0.5)
+        pts.add((x, y))
+        t += 0.125
+    rows = {}
+    for x, y in pts:
+        lo, hi = rows.get(y, (x, x))
+        rows[y] = (min(lo, x), max(hi, x))
+    return UniformConvexPsf([(y, rows[y][0], rows[y][1]) for y in sorted(rows)])
+
+
+def convex_zoo():
+    """Row-convex uniform PSFs with no compile-time span table: the paper's
+    discs and diagonals, lines at other angles, one-sided and wide / tall
+    extremes of the runtime-table kernel (kernels_spanr.cu)."""
+    z = {f"disc{d}": makeDiscPsf(d) for d in (2, 3, 5, 9, 17, 21, 31)}
+    for m in (5, 9, 17):
+        z[f"diag{m}"] = UniformConvexPsf([(dy, dy, dy) for dy in range(-(m // 2), m - m // 2)])
+    z["anti9"] = UniformConvexPsf([(dy, -dy, -dy) for dy in range(-4, 5)])
+    z["obl45_15"] = _oblique(15, 45.0)
+    z["obl60_25"] = _oblique(25, 60.0)
+    z["obl10_33"] = _oblique(33, 10.0)
+    z["right_only"] = UniformConvexPsf([(2, 3, 7), (3, 1, 9), (4, 4, 4)])
+    z["left_up"] = UniformConvexPsf([(-9, -12, -1), (-8, -20, -3)])
+    z["wide64"] = UniformConvexPsf([(0, -32, 32), (1, -10, 5)])
+    z["tall64"] = UniformConvexPsf([(dy, -1, 1) for dy in range(-32, 32)])
+    z["wide65"] = UniformConvexPsf([(0, -32, 33)])
+    z["tall65"] = UniformConvexPsf([(dy, 0, 0) for dy in range(-32, 33)])
+    return z
+
+
+@pytest.mark.parametrize("name", sorted(set(convex_zoo()) - {"wide65", "tall65"}))
+def test_runtime_span_table_kernel(name):
+    """GenericBox for any row-convex PSF runs the runtime span-table kernel,
+    parity with the oracle (which restates genericBoxInto) on awkward sizes;
+    also forced (spans mode 3) for the two compile-time shapes."""
+    psf = convex_zoo()[name]
+    assert ConvPlan(psf, K.GenericBox).engine() == "spans"
+    rng = np.random.default_rng(abs(hash(name)) % 2**31)
+    for h, w in [(1, 1), (1, 7), (5, 130), (70, 9), (33, 129), (131, 259), (300, 517)]:
+        img = rng.random((h, w)).astype(np.float32).astype(np.float64)
+        close(convolve(img, psf, K.GenericBox), O.convolve(img, psf, O.GENERIC_BOX))
+
+
+@pytest.mark.parametrize("name", ["disc10", "oblique"])
+def test_runtime_span_table_forced_on_baseline_shapes(name):
+    from paper_1304_7211_b200._lib import lib
+    psf = psf_zoo()[name]
+    prev = lib().fdg_set_option(b"spans", 3)
+    try:
+        rng = np.random.default_rng(21)
+        for h, w in [(3, 130), (131, 259), (517, 1030)]:
+            img = rng.random((h, w)).astype(np.float32).astype(np.float64)
+            close(convolve(img, psf, K.GenericBox), O.convolve(img, psf, O.GENERIC_BOX))
+    finally:
+        lib().fdg_set_option(b"spans", prev)
+
+
+@pytest.mark.parametrize("name", ["disc9", "disc17", "obl60_25", "diag9"])
+def test_runtime_span_table_rl(name):
+    """RL through the runtime-table kernel (fused quotient / update epilogues)."""
+    from paper_1304_7211_b200 import RlConfig, rlDeconvolve
+    psf = convex_zoo()[name]
+    g = W.scene(197, 143, 5, 8, 4) * 0.9 + 0.1
+    f = np.maximum(O.convolve(g, psf, O.GENERIC_BOX), 1e-6).astype(np.float32)
+    res = rlDeconvolve(f, psf, RlConfig(iterations=40, op=K.GenericBox))
+    ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, 40, O.GENERIC_BOX)
+    assert W.max_rel(res.image, ref) <= 1e-4
