@@ -261,17 +261,23 @@ def run_ours(args, cfg, world, rank, local):
 
     # ---- inputs (built once per rank, then resident in HBM)
     t0 = time.time()
-    fused_strips = world > 1 and cfg.batch == 1 and cfg.psf == "box15x15"  # the fused engine's PSF
+    strips = world > 1 and cfg.batch == 1  # row strips: libfdgpu's sharded runner (NCCL halo exchange)
+    shard = None
     if cfg.batch == 1:
-        halo = (S.fused_halo(psf) if fused_strips else S.psf_halo(psf)) if world > 1 else 0
-        s = S.strip_of(H_, world, rank, halo)
         f_full = make_input_gpu(cfg, psf, dev)
-        f_dev = torch.zeros((s.rows, pitch), dtype=torch.float32, device=dev)
-        f_dev[s.halo:s.halo + s.core, :W_] = f_full[s.r0:s.r0 + s.core]
-        f_host = f_full.cpu().numpy() if world == 1 else None
+        if strips:
+            ctx_sh = Context(local)
+            ctx_sh.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+            shard = S.ShardedRl(psf, rl_cfg, W_, H_, rank, world, S.comm_unique_id(), ctx=ctx_sh)
+            r0, core = shard.info["r0"], shard.info["core"]
+        else:
+            r0, core = 0, H_
+        f_dev = torch.zeros((core, pitch), dtype=torch.float32, device=dev)
+        f_dev[:, :W_] = f_full[r0:r0 + core]
+        f_host = f_full[r0:r0 + core].cpu().numpy() if world == 1 or strips else None
         del f_full
         nimg = 1
-        px_local = W_ * s.core
+        px_local = W_ * core
     else:
         share = S.batch_share(cfg.batch, world, rank)
         nimg = len(share)
@@ -281,28 +287,24 @@ def run_ours(args, cfg, world, rank, local):
         px_local = W_ * H_ * nimg
     setup_s = time.time() - t0
     u_dev = torch.empty_like(f_dev)
-    q_dev = torch.empty_like(f_dev)
-    solver = RlSolver(psf, rl_cfg, W_, s.core if s is not None else H_, batch=nimg, device=local)
     stream = torch.cuda.current_stream(dev)
-    solver.use_stream(stream.cuda_stream)
+    if shard is not None:
+        solver = None
 
-    if s is not None and world > 1 and fused_strips and solver.engine() == "fused":
-        fused = S.GpuFused(solver)
+        def step():  # per iteration: halo exchange (NCCL, comm stream) || interior, then the bands
+            shard.run(f_dev, u_dev, iters)
 
-        def step():  # one 2T-row u exchange + one fused launch per iteration
-            S.rl_strips_fused(f_dev, s, iters, fused, u=u_dev, u2=q_dev)
-    elif s is not None and world > 1:
-        passes = S.GpuPasses(solver)
-
-        def step():
-            S.rl_strips(f_dev, s, iters, passes, u=u_dev, q=q_dev)
+        def launch_count():
+            return shard.ctx.launch_count()
     else:
-        # one process, whole image(s): the C driver loop, replayed as a CUDA graph
-        f_run = f_dev[s.halo:s.halo + s.core] if s is not None else f_dev
-        u_run = u_dev[s.halo:s.halo + s.core] if s is not None else u_dev
+        solver = RlSolver(psf, rl_cfg, W_, H_, batch=nimg, device=local)
+        solver.use_stream(stream.cuda_stream)
 
-        def step():
-            solver.run(f_run, u_run, iters)
+        def step():  # one process, whole image(s): the C driver loop, replayed as a CUDA graph
+            solver.run(f_dev, u_dev, iters)
+
+        def launch_count():
+            return solver.launches()
 
     # ---- warmup
     for _ in range(args.warmup):
@@ -316,7 +318,7 @@ def run_ours(args, cfg, world, rank, local):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    launches0 = solver.launches()
+    launches0 = launch_count()
     ev[0].record(stream)
     for _ in range(args.steps):
         step()
@@ -325,7 +327,7 @@ def run_ours(args, cfg, world, rank, local):
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
-    launches = solver.launches() - launches0
+    launches = launch_count() - launches0
     ms_total = ev[0].elapsed_time(ev[1])
     if world > 1:
         t = torch.tensor([ms_total], device=dev)
@@ -343,9 +345,10 @@ def run_ours(args, cfg, world, rank, local):
     # iteration, or one row-resident launch per run); its average launch time
     # is the step time over the launches (incl. halo exchanges when world > 1)
     # (row strips on several ranks run the two-pass solver passes)
-    engine = solver.engine() if world == 1 or cfg.batch > 1 or fused_strips else ConvPlan(psf, op).engine()
+    engine = shard.info["engine"] if shard is not None else solver.engine()
     # launches of the dominant kernel per step (the step also has one tiny
-    # start-stamp kernel for the per-iteration trace)
+    # start-stamp kernel for the per-iteration trace; sharded runs add the
+    # boundary-band launches)
     per_step = {"fused": iters, "rowres": 1}.get(engine, 2 * iters)
     kern_ms = ms_step / per_step
     pxit_per_launch = px_local * iters / per_step
@@ -397,6 +400,26 @@ def run_ours(args, cfg, world, rank, local):
         e2e_s = statistics.median(e_t)
         e2e = {"value": W_ * H_ * iters / e2e_s / 1e6, "unit": "Mpx*it/s", "h2d_bytes_per_step": int(f_host.nbytes),
                "d2h_bytes_per_step": int(res.image.nbytes), "api": "paper_1304_7211_b200.rlDeconvolve (C ABI fdg_rl_deconvolve, host buffers)"}
+    elif shard is not None:
+        # this rank's strip through the sharded entry point with host buffers
+        # (H2D of its f rows, D2H of its u rows every step); max over ranks
+        f_pinned = torch.from_numpy(f_host).pin_memory().numpy()
+        u_pinned = torch.empty(f_host.shape, dtype=torch.float32).pin_memory().numpy()
+        for _ in range(2):
+            shard.run(f_pinned, u_pinned, iters)
+        e_t = []
+        for _ in range(max(1, min(args.steps, 3))):
+            dist.barrier()
+            a = time.perf_counter()
+            shard.run(f_pinned, u_pinned, iters)
+            e_t.append(time.perf_counter() - a)
+        tt = torch.tensor([statistics.median(e_t)], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        hb = torch.tensor([float(f_host.nbytes)], device=dev, dtype=torch.float64)
+        dist.all_reduce(hb)
+        e2e = {"value": W_ * H_ * iters / float(tt.item()) / 1e6, "unit": "Mpx*it/s",
+               "h2d_bytes_per_step": int(hb.item()), "d2h_bytes_per_step": int(hb.item()),
+               "api": "paper_1304_7211_b200.sharded.ShardedRl.run (C ABI fdg_shard_run, host buffers), max over ranks"}
     elif world == 1:
         # batch: per-image host API calls (pinned inputs), all images each step
         ctx = Context(local)
@@ -430,11 +453,16 @@ def run_ours(args, cfg, world, rank, local):
             "data": "synthetic (seeded BASELINE generator)",
             "config": workload_config(cfg, iters),
             "engine_info": {"engine": engine,
-                            "parallelism": (f"rowstrip{world}" + ("-fused" if fused_strips else ""))
-                            if cfg.batch == 1 else f"image-shard{world}",
+                            "parallelism": f"rowstrip{world}" if cfg.batch == 1 else f"image-shard{world}",
                             "l2": "working set 3 planes >> 126 MB L2 (no flush needed)" if W_ * H_ * 12 * nimg > 4e8
                             else "working set L2-resident (no flush: the RL loop re-reads its own planes)",
                             "setup_s": round(setup_s, 2)},
+            "sharding": ({"kind": "row strips, NCCL send/recv halo exchange on a comm stream overlapping the "
+                                  "strip interior (libfdgpu fdg_shard_run)",
+                          "halo_rows": shard.info["halo"],
+                          "exchanges_per_iteration": shard.info["exchanges_per_iteration"],
+                          "halo_bytes_per_iteration_rank0": shard.info["halo_bytes_per_iteration"]}
+                         if shard is not None else None),
             "per_gpu_value": value / world,
             "roofline": roof if roof else {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,

@@ -228,6 +228,50 @@ int fdg_mask_compact(fdg_ctx* ctx, const uint8_t* active, int width, int height,
                      int64_t* idx, int64_t idx_cap, int64_t* n_active, int32_t* runs,
                      int64_t runs_cap, int64_t* n_runs);
 
+/* ---- row-strip sharded RL --------------------------------
+ * One image of width x height split into `world` row strips, one per rank
+ * (one process per GPU).  Rank r owns rows [r*H/world, (r+1)*H/world) and
+ * runs the loop of rlDeconvolve (rl.hpp:153-177) on them; each iteration
+ * exchanges PSF-radius halo rows with ranks r-1 / r+1 through NCCL
+ * send/recv (NVLink), posted on a communication stream while the strip
+ * interior is computed, the two boundary bands following once the halo has
+ * landed.  Replicate clamping only at global rows 0 and H-1, so the result
+ * equals the single-GPU run.  Engines: "fused" (centred 15x15 box: one
+ * exchange of 2T rows per iteration), "rowres" (horizontal lines at dy = 0:
+ * rows independent, no exchange), else two passes with a T-row exchange of
+ * u and of q.  NCCL (libnccl.so.2) is loaded at run time (FDG_NCCL_LIB
+ * overrides the path); world == 1 needs no NCCL. */
+typedef struct fdg_shard fdg_shard;
+/* ncclGetUniqueId: rank 0 calls it and sends the 128 bytes to every rank */
+int fdg_comm_unique_id(unsigned char id[128]);
+/* this process's strip (rank of world; comm_id may be NULL when world == 1) */
+int fdg_shard_create(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg, int width, int height,
+                     int rank, int world, const unsigned char* comm_id, fdg_shard** out);
+/* `world` strips of one image in THIS process on ctx's device, the halo
+ * exchange done by device copies between them (tests / single-GPU
+ * measurement of the sharded schedule): out[0..world-1] */
+int fdg_shard_group_create(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg, int width,
+                           int height, int world, fdg_shard** out);
+void fdg_shard_destroy(fdg_shard* s);
+/* info[0..5] = first row, core rows, halo rows, exchanges per iteration,
+ * halo bytes sent per iteration, engine id (0 fused, 1 two-pass, 2 rowres) */
+int fdg_shard_info(const fdg_shard* s, long long info[6]);
+const char* fdg_shard_engine(const fdg_shard* s);
+/* RL on this rank's strip: f / u = its core rows (row r0 .. r0+core-1),
+ * host (host != 0) or device memory, row pitch `pitch` floats.  Device
+ * buffers and trace == NULL: asynchronous on ctx's stream.  trace (n =
+ * iterations): max|du| and NaN reduced over all ranks (one all-reduce at
+ * the end), seconds = this rank's device time per iteration. */
+int fdg_shard_run(fdg_shard* s, const float* f, float* u, int pitch, int host, int iterations,
+                  fdg_rl_record* trace);
+/* a group from fdg_shard_group_create: f / u = the whole image */
+int fdg_shard_group_run(fdg_shard** group, int world, const float* f, float* u, int pitch, int host,
+                        int iterations, fdg_rl_record* trace);
+/* device time of the last run's kernels per iteration, split: [0] interior
+ * launches, [1] boundary-band launches, [2] halo exchange (ms, summed over
+ * iterations; events on the launching streams) */
+int fdg_shard_timing(fdg_shard* s, double ms[3]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -133,6 +133,18 @@ def lib():
                                           C.c_int, C.c_int, C.c_int]),
             "fdg_solver_trace": (C.c_int, [vp, C.POINTER(RlRecordC), C.c_int]),
             "fdg_solver_reset_trace": (C.c_int, [vp]),
+            "fdg_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
+            "fdg_shard_create": (C.c_int, [vp, D, C.POINTER(RlConfigC), C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.POINTER(C.c_ubyte), C.POINTER(vp)]),
+            "fdg_shard_group_create": (C.c_int, [vp, D, C.POINTER(RlConfigC), C.c_int, C.c_int, C.c_int,
+                                                 C.POINTER(vp)]),
+            "fdg_shard_destroy": (None, [vp]),
+            "fdg_shard_info": (C.c_int, [vp, C.POINTER(C.c_longlong)]),
+            "fdg_shard_engine": (C.c_char_p, [vp]),
+            "fdg_shard_run": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(RlRecordC)]),
+            "fdg_shard_group_run": (C.c_int, [C.POINTER(vp), C.c_int, vp, vp, C.c_int, C.c_int, C.c_int,
+                                              C.POINTER(RlRecordC)]),
+            "fdg_shard_timing": (C.c_int, [vp, dp]),
             "fdg_mask_compact": (C.c_int, [vp, u8p, C.c_int, C.c_int, C.POINTER(C.c_int64), C.c_int64,
                                            C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.c_int64,
                                            C.POINTER(C.c_int64)]),

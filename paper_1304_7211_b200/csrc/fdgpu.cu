@@ -743,6 +743,9 @@ struct EventPool {
 
 }  // namespace
 
+int shard_set_loopback(int v);  // shard.cuh
+int shard_set_bands(int v);
+
 // =========================================================== ABI functions
 extern "C" {
 
@@ -754,6 +757,8 @@ int fdg_set_option(const char* name, int value) {
         set_fused_mode(value);
         return prev;
     }
+    if (name && std::strcmp(name, "shard_loopback") == 0) return shard_set_loopback(value);
+    if (name && std::strcmp(name, "shard_bands") == 0) return shard_set_bands(value);
     if (name && std::strcmp(name, "spans") == 0) {  // 0 auto, 1 tile kernel, 2 marching kernel
         const int prev = spans_mode();
         set_spans_mode(value);
@@ -1759,3 +1764,6 @@ int fdg_mask_compact(fdg_ctx* ctx, const uint8_t* active, int W, int H, int64_t*
 }
 
 }  // extern "C"
+
+// row-strip sharded RL (fdg_shard_*): uses the internals above
+#include "shard.cuh"

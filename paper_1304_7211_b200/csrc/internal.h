@@ -146,7 +146,8 @@ cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float
 bool fused_supported(int mx, int my, int min_dx, int min_dy);
 void set_fused_mode(int v);
 int fused_mode();
-// Output rows [y0, y1), reads clamped into [ylo, yhi] (the image edges; rows
+// Output rows [y0, y1) (and [y2, y3) when y3 > y2: the two boundary bands of
+// a row strip in one launch), reads clamped into [ylo, yhi] (the image edges; rows
 // between a shard's core and those edges must hold valid halo rows).
 // halo_in / halo_out: u_in / u_out are haloed planes (pitch_h, bstride_h;
 // fused_halo_left() / _right() replicated columns around each row; the
@@ -155,7 +156,15 @@ int fused_mode();
 cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int y0, int y1, int ylo,
                          int yhi, int batch, long long bstride, float scale, float eps, int clamp,
                          unsigned* maxchange, int* nanflag, unsigned long long* tend, cudaStream_t st,
-                         int halo_in = 0, int halo_out = 0, int pitch_h = 0, long long bstride_h = 0);
+                         int halo_in = 0, int halo_out = 0, int pitch_h = 0, long long bstride_h = 0,
+                         int y2 = 0, int y3 = 0);
+// The boundary bands of a row strip for the fused iteration (kernels_band.cu):
+// output rows [y0, y1) and [y2, y3) computed in place per 16 x 16 tile (no
+// row streaming), small enough to run next to the fused interior launch.
+cudaError_t launch_band(const float* u_in, int pitch_u, const float* f, int pitch_f, float* u_out, int pitch_o,
+                        int W, int y0, int y1, int y2, int y3, int ylo, int yhi, float scale, float eps, int clamp,
+                        int halo_out, int halo_l, int halo_r, unsigned* maxchange, int* nanflag,
+                        unsigned long long* tend, cudaStream_t st);
 int fused_halo_left();
 int fused_halo_right();
 bool fused_halo_ok(int W);

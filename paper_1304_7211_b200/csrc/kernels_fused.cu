@@ -74,6 +74,9 @@ struct FusedArgs {
     int pitch_u, pitch_o;  // row pitches of u_in / u_out
     long long bs_u, bs_o;  // image strides of u_in / u_out (batches)
     int y0, y1;    // output rows
+    int y2, y3;    // optional second output row range (plain grid only: both boundary bands of a
+                   // row strip in one launch); nb1 = CTA rows (blockIdx.y) of the first range
+    int nb1;
     int ylo, yhi;  // readable rows; replicate clamping at these (image) edges
     int band, batch;
     int lin_len, strips;  // lin_len > 0: work-balanced row ranges over the strips (batch 1)
@@ -615,13 +618,19 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     // resident CTA slot gets the same work (the plain grid leaves slots idle
     // when strips x bands < SMs x occupancy).  One call site of the segment
     // body keeps it inlined.
-    const int rows = a.y1 - a.y0;
+    int ybase = a.y0, rows = a.y1 - a.y0;
     long long p, end;
     if (a.lin_len > 0) {
         p = (long long)blockIdx.x * a.lin_len;
         end = min((long long)a.strips * rows, p + a.lin_len);
     } else {
-        p = (long long)blockIdx.x * rows + (long long)blockIdx.y * a.band;
+        int by = blockIdx.y;
+        if (by >= a.nb1) {  // second row range
+            by -= a.nb1;
+            ybase = a.y2;
+            rows = a.y3 - a.y2;
+        }
+        p = (long long)blockIdx.x * rows + (long long)by * a.band;
         end = min((long long)blockIdx.x * rows + rows, p + a.band);
     }
     for (bool first = true; p < end; first = false) {
@@ -633,7 +642,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         // strip reaching far past column W-1 makes the producer replicate
         // hundreds of columns per row and straggles the whole launch
         const int xs = a.W > G::CW ? min(sx * G::CW, (a.W - G::CW + 3) & ~3) : 0;
-        run_segment(xs, a.y0 + r0, a.y0 + r1);
+        run_segment(xs, ybase + r0, ybase + r1);
         p += r1 - r0;
     }
 #ifdef FDG_FUSED_PROBE
@@ -699,7 +708,13 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     const long long ctas_y = std::min(per_wave, std::max(1LL, (long long)rows / (4 * G::MY)));
     a.band = (int)((rows + ctas_y - 1) / ctas_y);
     if (const char* e = getenv("FDG_FUSED_BAND")) a.band = std::max(1, atoi(e));
-    dim3 grid(strips, (rows + a.band - 1) / a.band, a.batch);
+    a.nb1 = (rows + a.band - 1) / a.band;
+    const int rows2 = a.y3 - a.y2;
+    if (rows2 > 0) {  // both ranges with one band height (boundary bands: one CTA row each)
+        a.band = std::max(a.band, rows2);
+        a.nb1 = (rows + a.band - 1) / a.band;
+    }
+    dim3 grid(strips, a.nb1 + (rows2 > 0 ? (rows2 + a.band - 1) / a.band : 0), a.batch);
     // single images: spread (strip, row) work evenly over every resident CTA
     // slot when the plain grid leaves slots idle (config 4: 34 strips x 8
     // bands = 272 of 296 slots)
@@ -707,7 +722,7 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     a.lin_len = 0;
     a.strips = strips;
     const long long slots = (long long)sms * occ;
-    if (lin_on && a.batch == 1 && grid.x * grid.y < slots) {
+    if (lin_on && rows2 <= 0 && a.batch == 1 && grid.x * grid.y < slots) {
         const long long total = (long long)strips * rows;
         const long long L = (total + slots - 1) / slots;
         if (L >= 8 * G::MY) {
@@ -770,8 +785,11 @@ cudaError_t launch_pad_halo(const float* src, int pitch_src, long long bs_src, f
 cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int y0, int y1, int ylo,
                          int yhi, int batch, long long bstride, float scale, float eps, int clamp, unsigned* maxchange, int* nanflag,
                          unsigned long long* tend, cudaStream_t st, int halo_in, int halo_out, int pitch_h,
-                         long long bstride_h) {
+                         long long bstride_h, int y2, int y3) {
     FusedArgs a;
+    a.y2 = y2;
+    a.y3 = y3;
+    a.nb1 = 1 << 30;
     a.halo_in = halo_in;
     a.halo_out = halo_out;
     a.pitch_u = halo_in ? pitch_h : pitch;  // haloed planes share one pitch

@@ -228,3 +228,162 @@ def gather_strips(u: torch.Tensor, s: Strip, width: int, group=None) -> Optional
 def batch_share(batch: int, world: int, rank: int) -> range:
     """Images of a batch owned by `rank` (by-image sharding, no collective)."""
     return range(rank * batch // world, (rank + 1) * batch // world)
+
+
+# ------------------------------------------------------------------------
+# Native sharded loop (libfdgpu fdg_shard_*): the schedule above -- halo
+# exchange on a communication stream overlapping the strip interior, both
+# boundary bands in one launch -- with NCCL send/recv issued from C++
+# (include/fdgpu.h, csrc/shard.cuh).  torch.distributed only carries the
+# 128-byte NCCL unique id to the ranks.
+
+ENGINES = {0: "fused", 1: "two-pass", 2: "rowres"}
+
+
+def comm_unique_id(group=None) -> bytes:
+    """Rank 0 creates the NCCL unique id, every rank receives it."""
+    import ctypes as C
+
+    from ._lib import check, lib
+    obj = [None]
+    if dist.get_rank(group) == 0:
+        buf = (C.c_ubyte * 128)()
+        check(lib().fdg_comm_unique_id(buf))
+        obj[0] = bytes(buf)
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
+def _ptr_pitch(a, width):
+    """(pointer, pitch, host) of a torch CUDA tensor or a host numpy array."""
+    import numpy as np
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float32 or not a.flags.c_contiguous:
+            raise TypeError("host images must be C-contiguous float32")
+        return a.ctypes.data, a.shape[-1], 1
+    if not a.is_cuda or a.dtype != torch.float32 or a.stride(-1) != 1:
+        raise TypeError("device images must be float32 CUDA tensors with unit column stride")
+    return a.data_ptr(), a.stride(0), 0
+
+
+class _ShardBase:
+    def _info(self, h):
+        import ctypes as C
+
+        from ._lib import check, lib
+        v = (C.c_longlong * 6)()
+        check(lib().fdg_shard_info(h, v))
+        return {"r0": v[0], "core": v[1], "halo": v[2], "exchanges_per_iteration": v[3],
+                "halo_bytes_per_iteration": v[4], "engine": lib().fdg_shard_engine(h).decode()}
+
+    def _timing(self, h):
+        import ctypes as C
+
+        from ._lib import check, lib
+        ms = (C.c_double * 3)()
+        check(lib().fdg_shard_timing(h, ms))
+        return {"interior_ms": ms[0], "bands_ms": ms[1], "exchange_ms": ms[2]}
+
+    @staticmethod
+    def _records(trace, n):
+        if not trace:
+            return None
+        from ._lib import RlRecordC
+        return (RlRecordC * max(n, 1))()
+
+    @staticmethod
+    def _trace(recs, n):
+        if recs is None:
+            return None
+        from .rl import RlIterationRecord
+        return [RlIterationRecord(recs[i].iteration, recs[i].inactive_fraction, recs[i].max_abs_change,
+                                  recs[i].seconds) for i in range(n)]
+
+
+class ShardedRl(_ShardBase):
+    """This rank's row strip of one image (fdg_shard_create / _run)."""
+
+    def __init__(self, psf, cfg, width: int, height: int, rank: int, world: int, comm_id: Optional[bytes] = None,
+                 ctx=None):
+        import ctypes as C
+
+        from ._lib import Context, Desc, check, lib
+        self.ctx = ctx or Context.default()
+        self.cfg = cfg
+        self.width, self.height = width, height
+        idp = None
+        if comm_id is not None:
+            idp = (C.c_ubyte * 128).from_buffer_copy(comm_id)
+        h = C.c_void_p()
+        c = cfg.c()
+        check(lib().fdg_shard_create(self.ctx.h, Desc(psf).ref, C.byref(c), width, height, rank, world, idp,
+                                     C.byref(h)))
+        self.h = h
+        self.info = self._info(h)
+
+    def run(self, f, u, iterations: Optional[int] = None, trace: bool = False):
+        """f / u: this rank's core rows (host float32 arrays or CUDA
+        tensors).  Device buffers without trace: asynchronous on the
+        context's stream."""
+        from ._lib import check, lib
+        it = self.cfg.iterations if iterations is None else iterations
+        pf, pitch, host = _ptr_pitch(f, self.width)
+        pu, pitch_u, host_u = _ptr_pitch(u, self.width)
+        if (pitch, host) != (pitch_u, host_u):
+            raise ValueError("f and u need the same pitch and memory kind")
+        recs = self._records(trace, it)
+        check(lib().fdg_shard_run(self.h, pf, pu, pitch, host, it, recs))
+        return self._trace(recs, it)
+
+    def timing(self):
+        return self._timing(self.h)
+
+    def __del__(self):
+        try:
+            from ._lib import lib
+            if self.h:
+                lib().fdg_shard_destroy(self.h)
+        except Exception:
+            pass
+
+
+class ShardGroup(_ShardBase):
+    """`world` strips of one image in this process on one device, exchanging
+    halos by device copies (fdg_shard_group_*): the sharded schedule and row
+    ranges, checkable against the single-image run on one GPU."""
+
+    def __init__(self, psf, cfg, width: int, height: int, world: int, ctx=None):
+        import ctypes as C
+
+        from ._lib import Context, Desc, check, lib
+        self.ctx = ctx or Context.default()
+        self.cfg = cfg
+        self.width, self.height, self.world = width, height, world
+        arr = (C.c_void_p * world)()
+        c = cfg.c()
+        check(lib().fdg_shard_group_create(self.ctx.h, Desc(psf).ref, C.byref(c), width, height, world, arr))
+        self.arr = arr
+        self.infos = [self._info(arr[r]) for r in range(world)]
+
+    def run(self, f, u, iterations: Optional[int] = None, trace: bool = False):
+        from ._lib import check, lib
+        it = self.cfg.iterations if iterations is None else iterations
+        pf, pitch, host = _ptr_pitch(f, self.width)
+        pu, pitch_u, host_u = _ptr_pitch(u, self.width)
+        if (pitch, host) != (pitch_u, host_u):
+            raise ValueError("f and u need the same pitch and memory kind")
+        recs = self._records(trace, it)
+        check(lib().fdg_shard_group_run(self.arr, self.world, pf, pu, pitch, host, it, recs))
+        return self._trace(recs, it)
+
+    def timing(self, rank: int):
+        return self._timing(self.arr[rank])
+
+    def __del__(self):
+        try:
+            from ._lib import lib
+            for r in range(self.world):
+                if self.arr[r]:
+                    lib().fdg_shard_destroy(self.arr[r])
+        except Exception:
+            pass
