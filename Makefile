@@ -26,6 +26,11 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
 ORACLE    := oracle/liboracle.so
 REFLIB    := oracle/_ref/libfdref.so
 DROPIN    := tests/cpp/dropin_test
+# the reference's own acceptance suite (proj/tests/acceptance.cpp, compiled
+# where it lies) built against OUR drop-in headers and libfdgpu; the CLI
+# criterion (9) needs the reference CLI, which does not build here (CLI11)
+ACCEPT    := tests/cpp/acceptance_gpu
+REF_TESTS ?= $(REF_INC)/../tests
 
 HAVE_REF  := $(wildcard $(REF_INC)/fastdeconv/rl.hpp)
 
@@ -34,7 +39,7 @@ all: lib oracle $(if $(HAVE_REF),ref cpptests)
 lib: $(LIB)
 oracle: $(ORACLE)
 ref: $(REFLIB)
-cpptests: $(DROPIN)
+cpptests: $(DROPIN) $(ACCEPT)
 
 # one object per source (parallel with make -j); objects live in build/
 OBJS      := $(patsubst $(PKG)/csrc/%,build/%.o,$(CSRC))
@@ -63,8 +68,12 @@ $(DROPIN): tests/cpp/dropin_test.cpp include/fastdeconv/convolve.hpp include/fas
 	    -L$(PKG) -lfdgpu -Loracle -loracle -Wl,-rpath,'$$ORIGIN/../../$(PKG)' \
 	    -Wl,-rpath,'$$ORIGIN/../../oracle' -fopenmp
 
+$(ACCEPT): $(REF_TESTS)/acceptance.cpp include/fastdeconv/convolve.hpp include/fastdeconv/rl.hpp include/fdgpu.h $(LIB)
+	$(HOSTCXX) -std=c++20 -O2 -Iinclude -I$(REF_INC) -I$(REF_TESTS) -DFASTDECONV_CLI_PATH='"/bin/false"' \
+	    -o $@ $(REF_TESTS)/acceptance.cpp -L$(PKG) -lfdgpu -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
 clean:
-	rm -f $(LIB) $(ORACLE) $(REFLIB) $(DROPIN)
+	rm -f $(LIB) $(ORACLE) $(REFLIB) $(DROPIN) $(ACCEPT)
 	rm -rf build
 
 .PHONY: all lib oracle ref cpptests clean

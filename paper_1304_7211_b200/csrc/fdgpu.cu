@@ -125,6 +125,11 @@ struct DevScope {
 };
 }  // namespace
 
+namespace {
+struct SelCache;
+void sel_destroy(SelCache* c);
+}  // namespace
+
 struct fdg_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -148,6 +153,9 @@ struct fdg_ctx {
     // captured CUDA graph of the iteration loop) keyed by PSF, config and size
     fdg_solver* rl_solver = nullptr;
     std::string rl_key;
+    // rlDeconvolveSelective likewise keeps its buffers and the captured
+    // graph of the whole thinned loop (calls without mask replay / record)
+    SelCache* sel = nullptr;
     ~fdg_ctx();
 };
 
@@ -234,6 +242,7 @@ fdg_ctx::~fdg_ctx() {
     ds.enter(device);
     if (stream) cudaStreamSynchronize(stream);
     fdg_solver_destroy(rl_solver);
+    sel_destroy(sel);
     if (own_stream) cudaStreamDestroy(stream);
     a.release(), b.release(), c.release(), d.release(), m.release();
     tr_max.release(), tr_nan.release(), tr_inact.release(), first_bad.release(), tr_time.release();
@@ -1517,6 +1526,194 @@ int fdg_rl_step_planned(fdg_ctx* ctx, const fdg_plan* forward, const fdg_plan* a
     return rl_step_impl(ctx, forward, adjoint, cfg, u, f, W, H, u_out, max_abs_change);
 }
 
+}  // extern "C"
+
+namespace {
+// Selective RL with its buffers and the CUDA graph of the whole thinned loop
+// kept across calls (same PSF, config, threshold, period, thin_start, size
+// and engine options): a repeated call is H2D(f), one graph launch, D2H(u)
+// and the trace copies.  Per-iteration seconds come from device stamps
+// written by each iteration's last pass (rl.hpp:154,172).
+struct SelCache {
+    std::string key;
+    std::unique_ptr<fdg_plan> fwd, adj;
+    int W = 0, H = 0, pitch = 0, iters = 0;
+    DevBuf<float> df, du, dq, dv;
+    DevBuf<uint8_t> dm;
+    DevBuf<unsigned> mc;
+    DevBuf<int> nf;
+    DevBuf<unsigned long long> ni, ts;
+    DevBuf<int> tile_blocks, tile_count;  // own copies: the graph must not see a context buffer move
+    cudaGraphExec_t gexec = nullptr;
+    uint64_t g_launches = 0;
+    cudaStream_t gstream = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    int device = 0;
+    ~SelCache() {
+        DevScope ds;
+        ds.enter(device);
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (ev_in) cudaEventDestroy(ev_in);
+        if (ev_out) cudaEventDestroy(ev_out);
+        if (gstream) cudaStreamDestroy(gstream);
+    }
+};
+void sel_destroy(SelCache* c) { delete c; }
+
+int selective_cached(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, int kind, double threshold,
+                     int period, int thin_start, const float* f, int W, int H, float* u_out, fdg_rl_record* trace) {
+    int st;
+    fdg_rl_config c2 = *cfg;
+    c2.op = kind;
+    std::string key = rl_cache_key(desc, &c2, W, H);
+    key.append(reinterpret_cast<const char*>(&threshold), sizeof threshold);
+    key.append(reinterpret_cast<const char*>(&period), sizeof period);
+    key.append(reinterpret_cast<const char*>(&thin_start), sizeof thin_start);
+    SelCache* sc = ctx->sel;
+    if (!sc || sc->key != key) {
+        sel_destroy(ctx->sel);
+        ctx->sel = nullptr;
+        auto n = std::make_unique<SelCache>();
+        n->device = ctx->device;
+        if ((st = make_rl_plans(ctx, desc, kind, &n->fwd, &n->adj))) return st;
+        n->W = W;
+        n->H = H;
+        n->pitch = pitch_for(W);
+        n->iters = cfg->iterations;
+        const size_t np = (size_t)n->pitch * H;
+        CK(n->df.ensure(np));
+        CK(n->du.ensure(np));
+        CK(n->dq.ensure(np));
+        CK(n->dv.ensure(np));
+        CK(n->dm.ensure(np));
+        CK(n->mc.ensure(n->iters + 1));
+        CK(n->nf.ensure(n->iters + 1));
+        CK(n->ni.ensure(n->iters + 1));
+        CK(n->ts.ensure(n->iters + 2));
+        CK(cudaStreamCreateWithFlags(&n->gstream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&n->ev_in, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&n->ev_out, cudaEventDisableTiming));
+        n->key = std::move(key);
+        sc = ctx->sel = n.release();
+    }
+    const int iters = sc->iters, pitch = sc->pitch;
+    const size_t n = (size_t)pitch * H;
+    cudaStream_t user = ctx->stream;
+    if ((st = h2d(ctx->stg, sc->df.p, pitch, f, W, H, user))) return st;
+    const bool dense = sc->fwd->dev.engine == ENG_DENSE;
+    auto issue = [&]() -> int {
+        cudaStream_t s = ctx->stream;
+        CK(cudaMemsetAsync(sc->mc.p, 0, sizeof(unsigned) * (iters + 1), s));
+        CK(cudaMemsetAsync(sc->nf.p, 0, sizeof(int) * (iters + 1), s));
+        CK(cudaMemsetAsync(sc->ni.p, 0, sizeof(unsigned long long) * (iters + 1), s));
+        CK(cudaMemsetAsync(sc->ts.p, 0, sizeof(unsigned long long) * (iters + 2), s));
+        CK(cudaMemsetAsync(sc->dv.p, 0, n * sizeof(float), s));  // cachedV = 0 (rl.hpp:212)
+        CK(cudaMemcpyAsync(sc->du.p, sc->df.p, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        CK(launch_quot_const(sc->df.p, sc->dq.p, W, H, pitch, 0, 1, 0.f, (float)cfg->epsilon_div, s));
+        CK(launch_stamp(sc->ts.p, s));
+        ctx->launches += 2;
+        for (int k = 0; k < iters; ++k) {
+            if (k % period == 0) {  // reactivation (rl.hpp:219); k = 0: the initial all-active mask
+                CK(launch_fill_u8(sc->dm.p, 1, n, s));
+                ctx->launches += 1;
+            }
+            Epi e1;
+            e1.mode = EPI_MQUOT;
+            e1.aux = sc->df.p;
+            e1.out2 = sc->dv.p;
+            e1.eps = (float)cfg->epsilon_div;
+            e1.active = sc->dm.p;
+            if (dense) {
+                const DenseTiling t = dense_tiling(W, H);
+                const size_t tiles = (size_t)t.tiles_x * t.tiles_y;
+                CK(sc->tile_blocks.ensure(tiles * 256));
+                CK(sc->tile_count.ensure(tiles));
+                CK(launch_tile_compact(sc->dm.p, W, H, pitch, sc->tile_blocks.p, sc->tile_count.p, sc->ni.p + k, s));
+                CK(launch_dense(sc->fwd->dev, whole(sc->du.p, sc->dq.p, pitch, W, H), e1, s, sc->tile_blocks.p,
+                                sc->tile_count.p));
+                ctx->launches += 2;
+            } else {
+                CK(launch_count_inactive(sc->dm.p, n, sc->ni.p + k, s));
+                ctx->launches += 1;
+                if ((st = run_pass(ctx, sc->fwd.get(), whole(sc->du.p, sc->dq.p, pitch, W, H), e1, s))) return st;
+            }
+            Epi e2;
+            e2.mode = EPI_MUPDATE;
+            e2.aux = sc->du.p;
+            e2.clamp = cfg->clamp_nonnegative;
+            e2.maxchange = sc->mc.p + k;
+            e2.nanflag = sc->nf.p + k;
+            e2.tend = sc->ts.p + 1 + k;
+            e2.active = sc->dm.p;
+            e2.thr = (float)threshold;
+            e2.may_thin = k >= thin_start ? 1 : 0;
+            if (dense) {
+                CK(launch_dense(sc->adj->dev, whole(sc->dq.p, sc->du.p, pitch, W, H), e2, s, sc->tile_blocks.p,
+                                sc->tile_count.p));
+                ctx->launches += 1;
+            } else if ((st = run_pass(ctx, sc->adj.get(), whole(sc->dq.p, sc->du.p, pitch, W, H), e2, s))) {
+                return st;
+            }
+        }
+        return FDG_OK;
+    };
+    if (!sc->gexec) {
+        // first call: eager (kernel attributes, errors with their origin), then capture
+        const uint64_t before = ctx->launches;
+        if ((st = issue())) return st;
+        cudaGraph_t graph = nullptr;
+        ctx->stream = sc->gstream;
+        CK(cudaEventRecord(sc->ev_in, user));
+        CK(cudaStreamWaitEvent(sc->gstream, sc->ev_in, 0));
+        cudaError_t ce = cudaStreamBeginCapture(sc->gstream, cudaStreamCaptureModeThreadLocal);
+        const uint64_t cap0 = ctx->launches;
+        if (ce == cudaSuccess) st = issue();
+        cudaError_t ce2 = cudaStreamEndCapture(sc->gstream, &graph);
+        ctx->stream = user;
+        if (ce != cudaSuccess) return cuda_err(ce, "cudaStreamBeginCapture");
+        if (st) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (ce2 != cudaSuccess) return cuda_err(ce2, "cudaStreamEndCapture");
+        ce = cudaGraphInstantiate(&sc->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) return cuda_err(ce, "cudaGraphInstantiate");
+        sc->g_launches = ctx->launches - cap0;
+        ctx->launches = before + sc->g_launches;
+    } else {
+        CK(cudaEventRecord(sc->ev_in, user));
+        CK(cudaStreamWaitEvent(sc->gstream, sc->ev_in, 0));
+        CK(cudaGraphLaunch(sc->gexec, sc->gstream));
+        CK(cudaEventRecord(sc->ev_out, sc->gstream));
+        CK(cudaStreamWaitEvent(user, sc->ev_out, 0));
+        ctx->launches += sc->g_launches;
+    }
+    prefault(u_out, (size_t)W * H * sizeof(float));
+    if ((st = d2h(ctx->stg, u_out, sc->du.p, pitch, W, H, user))) return st;
+    std::vector<unsigned> hmc(iters);
+    std::vector<int> hnf(iters);
+    std::vector<unsigned long long> hni(iters), hts(iters + 1);
+    CK(cudaMemcpyAsync(hmc.data(), sc->mc.p, sizeof(unsigned) * iters, cudaMemcpyDeviceToHost, user));
+    CK(cudaMemcpyAsync(hnf.data(), sc->nf.p, sizeof(int) * iters, cudaMemcpyDeviceToHost, user));
+    CK(cudaMemcpyAsync(hni.data(), sc->ni.p, sizeof(unsigned long long) * iters, cudaMemcpyDeviceToHost, user));
+    CK(cudaMemcpyAsync(hts.data(), sc->ts.p, sizeof(unsigned long long) * (iters + 1), cudaMemcpyDeviceToHost, user));
+    CK(cudaStreamSynchronize(user));
+    const std::vector<double> sec = trace_seconds(hts, {}, iters);
+    for (int k = 0; k < iters; ++k) {
+        if (hnf[k])
+            return set_err(FDG_ENAN, "rlDeconvolveSelective: NaN in iterate at iteration " + std::to_string(k + 1));
+        if (trace) {
+            float m;
+            std::memcpy(&m, &hmc[k], sizeof m);
+            trace[k] = {k + 1, (double)hni[k] / ((double)W * H), (double)m, sec[k]};
+        }
+    }
+    return FDG_OK;
+}
+}  // namespace
+
+extern "C" {
 int fdg_rl_deconvolve_selective(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, double threshold,
                                 int period, int thin_start, const uint8_t* mask_replay, uint8_t* mask_record,
                                 const float* f, int W, int H, float* u_out, fdg_rl_record* trace) {
@@ -1531,6 +1728,9 @@ int fdg_rl_deconvolve_selective(fdg_ctx* ctx, const fdg_psf_desc* desc, const fd
         return set_err(FDG_EINVAL, "operator does not support masked evaluation");
     Entry en;
     if ((st = enter(ctx, en))) return st;
+    static const bool no_cache = getenv("FDG_NO_RL_CACHE") != nullptr;
+    if (!mask_replay && !mask_record && !no_cache && cfg->iterations >= 1)
+        return selective_cached(ctx, desc, cfg, kind, threshold, period, thin_start, f, W, H, u_out, trace);
     std::unique_ptr<fdg_plan> fwd, adj;
     if ((st = make_rl_plans(ctx, desc, kind, &fwd, &adj))) return st;
     const int iters = cfg->iterations;

@@ -70,17 +70,39 @@ __global__ void __launch_bounds__(256) k_taps(const TapsArgs a) {
         }
         tile[i] = in[(long long)gy * a.pitch + gx];
     }
+    // masked (thinned) evaluation: compact the tile's active pixels into a
+    // shared list first, so the work scales with active pixels, not with
+    // the tile (convolve.hpp:473-510 walks the active runs)
+    __shared__ int s_n;
+    __shared__ short s_list[TT_W * TT_H];
+    if (MASKED) {
+        if (tid == 0) s_n = 0;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int ly = threadIdx.y + 8 * (k >> 1), lx = threadIdx.x + 32 * (k & 1);
+            const int y = oy0 + ly, x = ox0 + lx;
+            if (y < a.y1 && x < a.W && a.e.active[img + (long long)y * a.pitch + x])
+                s_list[atomicAdd(&s_n, 1)] = (short)(ly * TT_W + lx);
+        }
+    }
     __syncthreads();
     TraceAcc tr;
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-            const int ly = threadIdx.y + 8 * rr, lx = threadIdx.x + 32 * cc;
+    const int nwork = MASKED ? s_n : 4 * 256;
+    for (int w = tid; w < nwork; w += 256) {
+        {
+            int ly, lx;
+            if (MASKED) {
+                ly = s_list[w] / TT_W;
+                lx = s_list[w] - ly * TT_W;
+            } else {  // the fixed 2 x 2 assignment: rows ty, ty + 8, columns tx, tx + 32
+                const int k = w >> 8;
+                ly = threadIdx.y + 8 * (k >> 1);
+                lx = threadIdx.x + 32 * (k & 1);
+            }
             const int y = oy0 + ly, x = ox0 + lx;
             if (y >= a.y1 || x >= a.W) continue;
             const long long idx = img + (long long)y * a.pitch + x;
-            if (MASKED && !a.e.active[idx]) continue;
             float acc = 0.f;
             for (int r = 0; r < a.nrows; ++r) {
                 const float* trow = tile + (ly + r) * a.tw + lx;
@@ -96,6 +118,7 @@ __global__ void __launch_bounds__(256) k_taps(const TapsArgs a) {
             if (a.uniform) acc *= a.scale;
             epilogue<MODE>(a.e, a.out, idx, acc, tr);
         }
+    }
     if (MODE == EPI_UPDATE || MODE == EPI_MUPDATE) trace_flush(a.e, tr);
 }
 
