@@ -87,17 +87,21 @@ __global__ void __launch_bounds__(BT_T) k_band(const BandArgs a) {
     // u tile: image rows clamp(yb0 - 14 + t), columns clamp(x0 - 14 + c);
     // f at the q positions (rows clamp(yb0 - 7 + r), columns clamp(x0 - 7 + j)).
     // Asynchronous 4-byte copies: every load of the CTA in flight at once.
-    for (int i = tid; i < ur * BT_UC; i += BT_T) {
-        const int t = i / BT_UC, c = i - t * BT_UC;
-        const int y = clampi(yb0 - 2 * BR_ + t, a.ylo, a.yhi);
-        const float* src = a.u_in + (long long)y * a.pitch_u + clampi(x0 - 2 * BR_ + c, 0, wm1);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&su[t][c])), "l"(src) : "memory");
+    // (one row per warp at a time: the row pointer and clamp once per row)
+    const int lane = tid & 31, wrp = tid >> 5;
+    for (int t = wrp; t < ur; t += BT_T / 32) {
+        const float* rp = a.u_in + (long long)clampi(yb0 - 2 * BR_ + t, a.ylo, a.yhi) * a.pitch_u;
+        for (int c = lane; c < BT_UC; c += 32) {
+            const float* src = rp + clampi(x0 - 2 * BR_ + c, 0, wm1);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&su[t][c])), "l"(src) : "memory");
+        }
     }
-    for (int i = tid; i < qr * BT_QC; i += BT_T) {
-        const int r = i / BT_QC, j = i - r * BT_QC;
-        const int yc = clampi(yb0 - BR_ + r, a.ylo, a.yhi);
-        const float* src = a.f + (long long)yc * a.pitch_f + clampi(x0 - BR_ + j, 0, wm1);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&sq[r][j])), "l"(src) : "memory");
+    for (int r = wrp; r < qr; r += BT_T / 32) {
+        const float* rp = a.f + (long long)clampi(yb0 - BR_ + r, a.ylo, a.yhi) * a.pitch_f;
+        for (int j = lane; j < BT_QC; j += 32) {
+            const float* src = rp + clampi(x0 - BR_ + j, 0, wm1);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&sq[r][j])), "l"(src) : "memory");
+        }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
