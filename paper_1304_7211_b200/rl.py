@@ -110,13 +110,22 @@ def _out(a, u32):
     return u32.astype(a.dtype if a.dtype in (np.float32, np.float64) else np.float64, copy=False)
 
 
-def rlDeconvolve(f, h, cfg: RlConfig = RlConfig(), ctx: Optional[Context] = None) -> RlResult:
-    """Standard RL from u0 = f (rl.hpp:140-179)."""
+def rlDeconvolve(f, h, cfg: RlConfig = RlConfig(), ctx: Optional[Context] = None,
+                 out: Optional[np.ndarray] = None) -> RlResult:
+    """Standard RL from u0 = f (rl.hpp:140-179).  ``out``: optional float32
+    C-contiguous (H, W) array that receives the result (e.g. page-locked
+    memory: the device -> host copy then runs at full DMA speed instead of
+    through the pinned staging chunks)."""
     a = _image(f)
     _validate(a, cfg, "rlDeconvolve")
     src = f32(a)
     hh, w = src.shape if src.size else (0, 0)
-    u = np.empty_like(src)
+    if out is not None:
+        if out.dtype != np.float32 or out.shape != src.shape or not out.flags.c_contiguous:
+            raise _lib.FdgInvalidArgument("rlDeconvolve: out must be a C-contiguous float32 array of the image's shape")
+        u = out
+    else:
+        u = np.empty_like(src)
     n = max(cfg.iterations, 0)
     recs = (RlRecordC * max(n, 1))()
     c = cfg.c()
