@@ -144,3 +144,50 @@ def test_strip_geometry():
     assert list(S.batch_share(64, 8, 3)) == list(range(24, 32))
     with pytest.raises(ValueError):
         S.strip_of(10, 4, 0, 7)
+
+
+# ---- the native sharded runner's host plumbing (libfdgpu fdg_shard_*)
+def _id_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cid = S.comm_unique_id()
+        ids = [None] * world
+        dist.all_gather_object(ids, cid)
+        if rank == 0:
+            q.put((len(cid), all(i == ids[0] for i in ids)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_comm_unique_id_reaches_every_rank():
+    """Rank 0's NCCL unique id (fdg_comm_unique_id) is what every rank
+    passes to fdg_shard_create (bench.py --gpus N)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    n, same = q.get(timeout=5)
+    assert n == 128 and same
+
+
+def test_shard_create_validation_before_device():
+    """Argument errors surface as the reference's exception class even without
+    a GPU; the compute entry point itself then refuses (no CPU fallback)."""
+    import ctypes as C
+
+    from paper_1304_7211_b200._lib import Desc, FdgError, FdgInvalidArgument, check, lib
+    from paper_1304_7211_b200.rl import RlConfig
+    h = C.c_void_p()
+    cfg = RlConfig(iterations=2).c()
+    psf = makeBoxPsf(15, 15)
+    with pytest.raises(FdgInvalidArgument, match="communicator"):
+        check(lib().fdg_shard_create(None, Desc(psf).ref, C.byref(cfg), 64, 64, 0, 2, None, C.byref(h)))
+    with pytest.raises(FdgError):
+        check(lib().fdg_shard_create(None, Desc(psf).ref, C.byref(cfg), 64, 64, 0, 1, None, C.byref(h)))
