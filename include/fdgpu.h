@@ -244,7 +244,9 @@ int fdg_mask_compact(fdg_ctx* ctx, const uint8_t* active, int width, int height,
 typedef struct fdg_shard fdg_shard;
 /* ncclGetUniqueId: rank 0 calls it and sends the 128 bytes to every rank */
 int fdg_comm_unique_id(unsigned char id[128]);
-/* this process's strip (rank of world; comm_id may be NULL when world == 1) */
+/* this process's strip (rank of world; comm_id may be NULL when world == 1;
+ * given with world == 1, a one-rank NCCL communicator carries the trace
+ * all-reduce) */
 int fdg_shard_create(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg, int width, int height,
                      int rank, int world, const unsigned char* comm_id, fdg_shard** out);
 /* `world` strips of one image in THIS process on ctx's device, the halo

@@ -532,10 +532,12 @@ __global__ void __launch_bounds__(32 * NTY, MINB) k_spant(const SpanArgs a) {
             const int r = tl - o;
             if (r < 0 || r >= NR) continue;
             const int lo = SH::LO(r) + E::XL, hi = SH::HI(r) + E::XL;
-            acc[o].x += Pf[hi] - (lo > 0 ? Pf[lo - 1] : 0.f);
-            acc[o].y += Pf[hi + 1] - Pf[lo];
-            acc[o].z += Pf[hi + 2] - Pf[lo + 1];
-            acc[o].w += Pf[hi + 3] - Pf[lo + 2];
+            // packed accumulate (FADD2, same rounding per lane): +3 % on configs 1 / 2
+            const float2 d01 = make_float2(Pf[hi] - (lo > 0 ? Pf[lo - 1] : 0.f), Pf[hi + 1] - Pf[lo]);
+            const float2 d23 = make_float2(Pf[hi + 2] - Pf[lo + 1], Pf[hi + 3] - Pf[lo + 2]);
+            const float2 a01 = __fadd2_rn(make_float2(acc[o].x, acc[o].y), d01);
+            const float2 a23 = __fadd2_rn(make_float2(acc[o].z, acc[o].w), d23);
+            acc[o] = make_float4(a01.x, a01.y, a23.x, a23.y);
         }
     }
     const int xc = x0 + 4 * tx;

@@ -520,7 +520,7 @@ int shard_epilogue(fdg_shard* s, float* u, int pitch, int host, int iters, cudaS
 }
 
 int shard_trace_out(fdg_shard* s, int iters, fdg_rl_record* trace, cudaStream_t st, bool reduce) {
-    if (reduce && s->world > 1 && s->group.empty() && !s->loopback) {
+    if (reduce && s->comm) {
         NcclApi& api = nccl_api();
         NK(api.all_reduce(s->mc.p, s->mc.p, (size_t)iters, NCCL_UINT32, NCCL_MAX, s->comm, st));
         NK(api.all_reduce(s->nf.p, s->nf.p, (size_t)iters, NCCL_UINT32, NCCL_MAX, s->comm, st));
@@ -572,7 +572,9 @@ int fdg_shard_create(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config*
     auto s = std::make_unique<fdg_shard>();
     if ((st = shard_init(s.get(), ctx, psf, cfg, width, height, rank, world))) return st;
     s->loopback = loop;
-    if (world > 1 && !loop) {
+    // a communicator whenever an id is given (world 1 too: the trace
+    // all-reduce then runs through NCCL on one GPU)
+    if (comm_id && !loop) {
         NcclApi& api = nccl_api();
         if (!api.ok) return set_err(FDG_ECUDA, api.err);
         nccl_unique_id u;

@@ -241,10 +241,16 @@ ENGINES = {0: "fused", 1: "two-pass", 2: "rowres"}
 
 
 def comm_unique_id(group=None) -> bytes:
-    """Rank 0 creates the NCCL unique id, every rank receives it."""
+    """Rank 0 creates the NCCL unique id, every rank receives it (without an
+    initialised process group: this process's own id, for a one-rank
+    communicator)."""
     import ctypes as C
 
     from ._lib import check, lib
+    if not dist.is_available() or not dist.is_initialized():
+        buf = (C.c_ubyte * 128)()
+        check(lib().fdg_comm_unique_id(buf))
+        return bytes(buf)
     obj = [None]
     if dist.get_rank(group) == 0:
         buf = (C.c_ubyte * 128)()

@@ -120,3 +120,21 @@ def test_nan_in_iterate_reported_by_the_group(psf, op):
     grp = ShardGroup(psf, RlConfig(iterations=30, op=op), 256, 192, 2)
     with pytest.raises(FdgNaNError, match=r"NaN in iterate at iteration \d+"):
         grp.run(f, np.empty_like(f), trace=True)
+
+
+def test_world1_with_nccl_communicator():
+    """A one-rank NCCL communicator (libnccl.so.2 loaded with dlopen, comm
+    init, the trace all-reduce) on the real GPU: the NCCL plumbing of the
+    sharded runner executes; the result equals the plain run."""
+    from paper_1304_7211_b200.sharded import comm_unique_id
+    psf = makeBoxPsf(15, 15)
+    w, h = 640, 300
+    _, f = _input(w, h, 9, psf, K.Box2dSliding)
+    cfg = RlConfig(iterations=8, op=K.Box2dSliding)
+    sh = ShardedRl(psf, cfg, w, h, 0, 1, comm_unique_id())
+    u = np.empty_like(f)
+    tr = sh.run(f, u, trace=True)
+    single = rlDeconvolve(f, psf, cfg)
+    np.testing.assert_allclose(u, single.image, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose([r.maxAbsChange for r in tr], [r.maxAbsChange for r in single.trace.records],
+                               rtol=1e-5)
