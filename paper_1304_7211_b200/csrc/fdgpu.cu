@@ -538,6 +538,18 @@ int run_fused(fdg_ctx* ctx, const fdg_plan* pl, const float* u_in, const float* 
                                  (float)cfg->epsilon_div, cfg->clamp_nonnegative, mc, nf, te, st, halo_in, halo_out,
                                  hp ? hp->pitch : 0, hp ? hp->stride : 0);
     if (r != cudaSuccess) return cuda_err(r, "fused RL iteration launch");
+    static const bool dbg = getenv("FDG_DEBUG_SYNC") != nullptr;  // diagnostics: fault at its launch
+    if (dbg) {
+        cudaStreamCaptureStatus cs;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+            r = cudaStreamSynchronize(st);
+            if (r != cudaSuccess) {
+                fprintf(stderr, "[fdg debug] fused launch W=%d H=%d y=[%d,%d) ylo=%d yhi=%d halo_in=%d halo_out=%d pitch=%d: %s\n",
+                        W, H, y0, y1, ylo, yhi, halo_in, halo_out, pitch, cudaGetErrorString(r));
+                return cuda_err(r, "fused RL iteration (debug sync)");
+            }
+        }
+    }
     ctx->launches += 1;
     return FDG_OK;
 }
@@ -1378,6 +1390,14 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     }
     Entry en;
     if ((st = enter(ctx, en))) return st;
+    static const bool dbg = getenv("FDG_DEBUG_SYNC") != nullptr;
+    if (dbg) {
+        cudaError_t e0 = cudaDeviceSynchronize();
+        if (e0 != cudaSuccess) {
+            fprintf(stderr, "[fdg debug] fault pending at rlDeconvolve entry (%dx%d): %s\n", W, H, cudaGetErrorString(e0));
+            return cuda_err(e0, "pending fault at entry (debug sync)");
+        }
+    }
     // Repeated calls with the same PSF / config / size / options replay the
     // solver's captured graph (one cudaGraphLaunch for the whole loop)
     static const bool no_cache = getenv("FDG_NO_RL_CACHE") != nullptr;

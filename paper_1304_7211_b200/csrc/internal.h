@@ -148,6 +148,8 @@ void set_fused_mode(int v);
 int fused_mode();
 // Output rows [y0, y1) (and [y2, y3) when y3 > y2: the two boundary bands of
 // a row strip in one launch), reads clamped into [ylo, yhi] (the image edges; rows
+// ... balanced = 0: the plain strip x band grid instead of work-balanced
+// segments (row strips of a sharded image: 145 vs 150 us per 2048-row strip)
 // between a shard's core and those edges must hold valid halo rows).
 // halo_in / halo_out: u_in / u_out are haloed planes (pitch_h, bstride_h;
 // fused_halo_left() / _right() replicated columns around each row; the
@@ -157,7 +159,7 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
                          int yhi, int batch, long long bstride, float scale, float eps, int clamp,
                          unsigned* maxchange, int* nanflag, unsigned long long* tend, cudaStream_t st,
                          int halo_in = 0, int halo_out = 0, int pitch_h = 0, long long bstride_h = 0,
-                         int y2 = 0, int y3 = 0);
+                         int y2 = 0, int y3 = 0, int balanced = 1);
 // The boundary bands of a row strip for the fused iteration (kernels_band.cu):
 // output rows [y0, y1) and [y2, y3) computed in place per 16 x 16 tile (no
 // row streaming), small enough to run next to the fused interior launch.

@@ -486,8 +486,9 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         float4 hlast = make_float4(0.f, 0.f, 0.f, 0.f);
         float maxd = 0.f;
         const uint64_t pol_first = HINT ? policy_evict_first() : 0;
-        auto load_u = [&](int o) {  // u of output o
-            const float* p = ucol + min(yb0 + o, yb1 - 1) * pitch_u;
+        auto load_u = [&](int o) {  // u of output o (o < 0: ring not yet full, the value is unused --
+                                     // clamp the row so a tiny image never reads before its plane)
+            const float* p = ucol + clampi(yb0 + o, yb0, yb1 - 1) * pitch_u;
             return HINT ? ldg4_hint(p, pol_first) : ldg4(p);
         };
         auto store = [&](auto fs, const int o, const float4 c, const float4 u) {
@@ -719,10 +720,11 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     // slot when the plain grid leaves slots idle (config 4: 34 strips x 8
     // bands = 272 of 296 slots)
     static const bool lin_on = !getenv("FDG_FUSED_LIN") || atoi(getenv("FDG_FUSED_LIN")) != 0;
-    a.lin_len = 0;
     a.strips = strips;
     const long long slots = (long long)sms * occ;
-    if (lin_on && rows2 <= 0 && a.batch == 1 && grid.x * grid.y < slots) {
+    const bool want_lin = a.lin_len >= 0;  // caller: -1 = plain grid
+    a.lin_len = 0;
+    if (lin_on && want_lin && rows2 <= 0 && a.batch == 1 && grid.x * grid.y < slots) {
         const long long total = (long long)strips * rows;
         const long long L = (total + slots - 1) / slots;
         if (L >= 8 * G::MY) {
@@ -785,8 +787,9 @@ cudaError_t launch_pad_halo(const float* src, int pitch_src, long long bs_src, f
 cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int y0, int y1, int ylo,
                          int yhi, int batch, long long bstride, float scale, float eps, int clamp, unsigned* maxchange, int* nanflag,
                          unsigned long long* tend, cudaStream_t st, int halo_in, int halo_out, int pitch_h,
-                         long long bstride_h, int y2, int y3) {
+                         long long bstride_h, int y2, int y3, int balanced) {
     FusedArgs a;
+    a.lin_len = balanced ? 0 : -1;
     a.y2 = y2;
     a.y3 = y3;
     a.nb1 = 1 << 30;

@@ -296,7 +296,7 @@ int shard_fused(fdg_shard* s, int k, int y0, int y1, int y2, int y3, cudaStream_
     cudaError_t r = launch_fused(src, s->f, dst, s->pitch, s->W, y0, y1, shard_ylo(s), shard_yhi(s), 1, 0,
                                  s->fwd->dev.scale, (float)s->cfg.epsilon_div, s->cfg.clamp_nonnegative,
                                  s->mc.p + slot, s->nf.p + slot, s->ts.p + 1 + slot, st, k > 0, 1, s->hp.pitch,
-                                 s->hp.stride, y2, y3);
+                                 s->hp.stride, y2, y3, s->world == 1);
     if (r != cudaSuccess) return cuda_err(r, "fused RL iteration launch (strip)");
     s->ctx->launches += 1;
     return FDG_OK;
