@@ -288,7 +288,9 @@ int shard_exchange(fdg_shard* s, int role, int rows, cudaStream_t st) {
     return FDG_OK;
 }
 
-// one fused iteration k over output rows [y0, y1) (+ [y2, y3))
+// one fused iteration k over output rows [y0, y1) (+ [y2, y3)); strips up to
+// ~3000 rows run the plain strip x band grid (measured at 16384 columns: 2048-row
+// strips 145 vs 150 us, 4096-row strips 266 vs 252 us with work-balanced segments)
 int shard_fused(fdg_shard* s, int k, int y0, int y1, int y2, int y3, cudaStream_t st) {
     const float* src = k == 0 ? s->f : (k & 1 ? s->uA : s->uB);
     float* dst = k & 1 ? s->uB : s->uA;
@@ -296,7 +298,7 @@ int shard_fused(fdg_shard* s, int k, int y0, int y1, int y2, int y3, cudaStream_
     cudaError_t r = launch_fused(src, s->f, dst, s->pitch, s->W, y0, y1, shard_ylo(s), shard_yhi(s), 1, 0,
                                  s->fwd->dev.scale, (float)s->cfg.epsilon_div, s->cfg.clamp_nonnegative,
                                  s->mc.p + slot, s->nf.p + slot, s->ts.p + 1 + slot, st, k > 0, 1, s->hp.pitch,
-                                 s->hp.stride, y2, y3, s->world == 1);
+                                 s->hp.stride, y2, y3, s->world == 1 || s->core > 3000);
     if (r != cudaSuccess) return cuda_err(r, "fused RL iteration launch (strip)");
     s->ctx->launches += 1;
     return FDG_OK;
