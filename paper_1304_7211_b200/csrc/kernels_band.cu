@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(BT_T) k_band(const BandArgs a) {
     __syncthreads();
     // q rows / columns beyond the readable rows / the image replicate the edge
     // (the second convolution pads its input, convolve.hpp:288-342)
-    {
+    if (yb0 - BR_ < a.ylo || yb1 - 1 + BR_ > a.yhi || x0 - BR_ < 0 || x0 + BT_QC - 1 - BR_ > wm1) {  // edge tiles only
         const int rlo = a.ylo - (yb0 - BR_), rhi = a.yhi - (yb0 - BR_);
         const int clo = -(x0 - BR_), chi = wm1 - (x0 - BR_);
         for (int i = tid; i < qr * BT_QC; i += BT_T) {
