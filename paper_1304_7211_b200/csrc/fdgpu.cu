@@ -366,6 +366,7 @@ int build_plan(fdg_ctx* ctx, const HostPsf& psf, int preference, std::unique_ptr
                 d.engine = ENG_SPANS;
                 d.uniform = 1;
                 d.scale = (float)u;
+                if (spans_jit_mode()) spans_jit_ready(d);  // compile its tile kernel now, not inside a capture
                 break;
             }
             std::vector<Tap> t;
@@ -776,6 +777,11 @@ int fdg_set_option(const char* name, int value) {
     if (name && std::strcmp(name, "fused") == 0) {
         const int prev = fused_mode();
         set_fused_mode(value);
+        return prev;
+    }
+    if (name && std::strcmp(name, "spans_jit") == 0) {  // 1: NVRTC tile kernels for span tables, 0: off
+        const int prev = spans_jit_mode();
+        set_spans_jit(value);
         return prev;
     }
     if (name && std::strcmp(name, "shard_loopback") == 0) return shard_set_loopback(value);

@@ -112,7 +112,13 @@ bool spans_supported(const DevPsf& p);
 // <= 64 rows and max_dx - min_dx <= 64
 bool spanr_supported(const DevPsf& p);
 cudaError_t launch_spanr(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st);
-// "tile" / "marching" (compile-time tables) or "runtime-table"
+// span tile kernel compiled at run time for a plan's table (spans_jit.cu,
+// NVRTC); ready() compiles on first use per table and device (plan build)
+bool spans_jit_ready(const DevPsf& p);
+cudaError_t launch_spans_jit(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st);
+void set_spans_jit(int v);
+int spans_jit_mode();
+// "tile" / "marching" (compile-time tables), "jit-tile" or "runtime-table"
 const char* spans_kernel(const DevPsf& p, long long px);
 // spans kernel choice: 0 = by image size (tile <= 4.5 Mpx per launch), 1 = tile, 2 = marching,
 // 3 = the runtime-table kernel for every shape

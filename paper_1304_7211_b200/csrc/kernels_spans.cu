@@ -706,6 +706,8 @@ cudaError_t launch_spans(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
     if (spans_mode() != 3) {
         if (same_shape<DiscR10>(p)) return launch_shape<DiscR10>(p, g, e, st);
         if (same_shape<Oblique21>(p)) return launch_shape<Oblique21>(p, g, e, st);
+        // any other table: the tile kernel compiled for it at plan time (NVRTC)
+        if (spans_jit_mode() && spans_jit_ready(p)) return launch_spans_jit(p, g, e, st);
     }
     return launch_spanr(p, g, e, st);
 }
@@ -715,6 +717,7 @@ const char* spans_kernel(const DevPsf& p, long long px) {
         const int mode = spans_mode();
         return (mode ? mode == 1 : px <= 4608ll * 1024) ? "tile" : "marching";
     }
+    if (spans_mode() != 3 && spans_jit_mode() && spans_jit_ready(p)) return "jit-tile";
     return "runtime-table";
 }
 

@@ -198,17 +198,24 @@ def convex_zoo():
     return z
 
 
+@pytest.mark.parametrize("jit", [1, 0])
 @pytest.mark.parametrize("name", sorted(set(convex_zoo()) - {"wide65", "tall65"}))
-def test_runtime_span_table_kernel(name):
-    """GenericBox for any row-convex PSF runs the runtime span-table kernel,
-    parity with the oracle (which restates genericBoxInto) on awkward sizes;
-    also forced (spans mode 3) for the two compile-time shapes."""
-    psf = convex_zoo()[name]
-    assert ConvPlan(psf, K.GenericBox).engine() == "spans"
-    rng = np.random.default_rng(abs(hash(name)) % 2**31)
-    for h, w in [(1, 1), (1, 7), (5, 130), (70, 9), (33, 129), (131, 259), (300, 517)]:
-        img = rng.random((h, w)).astype(np.float32).astype(np.float64)
-        close(convolve(img, psf, K.GenericBox), O.convolve(img, psf, O.GENERIC_BOX))
+def test_runtime_span_table_kernel(name, jit):
+    """GenericBox for any row-convex PSF: the tile kernel compiled for its
+    table at plan time (NVRTC, spans_jit.cu) and the runtime-table kernel
+    (kernels_spanr.cu), parity with the oracle (which restates
+    genericBoxInto) on awkward sizes."""
+    from paper_1304_7211_b200._lib import lib
+    prev = lib().fdg_set_option(b"spans_jit", jit)
+    try:
+        psf = convex_zoo()[name]
+        assert ConvPlan(psf, K.GenericBox).engine() == "spans"
+        rng = np.random.default_rng(abs(hash(name)) % 2**31)
+        for h, w in [(1, 1), (1, 7), (5, 130), (70, 9), (33, 129), (131, 259), (300, 517)]:
+            img = rng.random((h, w)).astype(np.float32).astype(np.float64)
+            close(convolve(img, psf, K.GenericBox), O.convolve(img, psf, O.GENERIC_BOX))
+    finally:
+        lib().fdg_set_option(b"spans_jit", prev)
 
 
 @pytest.mark.parametrize("name", ["disc10", "oblique"])
@@ -225,9 +232,21 @@ def test_runtime_span_table_forced_on_baseline_shapes(name):
         lib().fdg_set_option(b"spans", prev)
 
 
+@pytest.mark.parametrize("jit", [1, 0])
 @pytest.mark.parametrize("name", ["disc9", "disc17", "obl60_25", "diag9"])
-def test_runtime_span_table_rl(name):
-    """RL through the runtime-table kernel (fused quotient / update epilogues)."""
+def test_runtime_span_table_rl(name, jit):
+    """RL through the JIT tile kernel / the runtime-table kernel (fused
+    quotient / update epilogues)."""
+    from paper_1304_7211_b200 import RlConfig, rlDeconvolve
+    from paper_1304_7211_b200._lib import lib
+    prev = lib().fdg_set_option(b"spans_jit", jit)
+    try:
+        _span_rl(name)
+    finally:
+        lib().fdg_set_option(b"spans_jit", prev)
+
+
+def _span_rl(name):
     from paper_1304_7211_b200 import RlConfig, rlDeconvolve
     psf = convex_zoo()[name]
     g = W.scene(197, 143, 5, 8, 4) * 0.9 + 0.1
