@@ -68,8 +68,13 @@ __global__ void __launch_bounds__(256) k_taps(const TapsArgs a) {
             gy = clampi(gy, a.ylo, a.yhi);
             gx = clampi(gx, 0, a.W - 1);
         }
-        tile[i] = in[(long long)gy * a.pitch + gx];
+        // 4-byte cp.async: every load of the thread in flight at once (the
+        // dependent load -> store loop was ~5 serial global round trips)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(tile + i)),
+                     "l"(in + (long long)gy * a.pitch + gx)
+                     : "memory");
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     // masked (thinned) evaluation: compact the tile's active pixels into a
     // shared list first, so the work scales with active pixels, not with
     // the tile (convolve.hpp:473-510 walks the active runs)

@@ -78,10 +78,10 @@ __device__ __forceinline__ float epi1(float v, float x, float eps, int clamp, fl
     csum += value;
     return value;
 }
-template <int MODE>
+template <int MODE, int V, int NTY>
 __device__ void spant(const JitArgs& a) {
     using E = Ext<32>;
-    constexpr int NR = SH::NR, V = JV, NTY = JNTY;
+    constexpr int NR = SH::NR;
     constexpr int TW = 128, TH = V * NTY, TR = TH + NR - 1, TC = TW + E::HL + E::HR, TCP = TC + 4;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* tile = reinterpret_cast<float*>(smem_raw);
@@ -213,9 +213,14 @@ __device__ void spant(const JitArgs& a) {
         }
     }
 }
-extern "C" __global__ void __launch_bounds__(32 * JNTY, JMINB) spant_store(const JitArgs a) { spant<0>(a); }
-extern "C" __global__ void __launch_bounds__(32 * JNTY, JMINB) spant_quot(const JitArgs a) { spant<1>(a); }
-extern "C" __global__ void __launch_bounds__(32 * JNTY, JMINB) spant_update(const JitArgs a) { spant<2>(a); }
+// large images: JV x JNTY-row tiles; small images (latency bound, ~1 wave):
+// 2 x 4-row tiles, many more CTAs
+extern "C" __global__ void __launch_bounds__(32 * JNTY, JMINB) spant_store(const JitArgs a) { spant<0, JV, JNTY>(a); }
+extern "C" __global__ void __launch_bounds__(32 * JNTY, JMINB) spant_quot(const JitArgs a) { spant<1, JV, JNTY>(a); }
+extern "C" __global__ void __launch_bounds__(32 * JNTY, JMINB) spant_update(const JitArgs a) { spant<2, JV, JNTY>(a); }
+extern "C" __global__ void __launch_bounds__(128) spant_store_s(const JitArgs a) { spant<0, 2, 4>(a); }
+extern "C" __global__ void __launch_bounds__(128) spant_quot_s(const JitArgs a) { spant<1, 2, 4>(a); }
+extern "C" __global__ void __launch_bounds__(128) spant_update_s(const JitArgs a) { spant<2, 2, 4>(a); }
 )JIT";
 
 // host mirror of JitArgs (same layout)
@@ -291,10 +296,12 @@ Nvrtc& nvrtc() {
 
 struct JitKernel {
     bool ok = false;
-    CUfunction fn[3] = {nullptr, nullptr, nullptr};
+    CUfunction fn[3] = {nullptr, nullptr, nullptr};    // large-image tiles
+    CUfunction fns[3] = {nullptr, nullptr, nullptr};   // small-image tiles (2 x 4 rows)
     int V = 0, NTY = 0;
-    size_t smem = 0;
+    size_t smem = 0, smem_s = 0;
 };
+constexpr int JIT_SMALL_PX = 512 * 1024;  // images up to this many pixels per launch: small tiles
 
 std::atomic<int> g_jit{getenv("FDG_SPANS_JIT") ? atoi(getenv("FDG_SPANS_JIT")) : 1};
 std::mutex g_jit_mu;
@@ -360,11 +367,17 @@ JitKernel* jit_get(const DevPsf& p) {
     CUmodule mod = nullptr;
     if (n.module_load(&mod, cubin.data()) != CUDA_SUCCESS) return nullptr;
     const char* names[3] = {"spant_store", "spant_quot", "spant_update"};
-    const int TR = V * NTY + p.nrows - 1, TCP = 128 + (xl + 3) / 4 * 4 + (xr + 3) / 4 * 4 + 4;
-    out->smem = sizeof(float) * (size_t)TR * TCP;
+    const char* names_s[3] = {"spant_store_s", "spant_quot_s", "spant_update_s"};
+    const int TCP = 128 + (xl + 3) / 4 * 4 + (xr + 3) / 4 * 4 + 4;
+    out->smem = sizeof(float) * (size_t)(V * NTY + p.nrows - 1) * TCP;
+    out->smem_s = sizeof(float) * (size_t)(2 * 4 + p.nrows - 1) * TCP;
     for (int m = 0; m < 3; ++m) {
         if (n.get_function(&out->fn[m], mod, names[m]) != CUDA_SUCCESS) return nullptr;
         if (n.func_set_attr(out->fn[m], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)out->smem) !=
+            CUDA_SUCCESS)
+            return nullptr;
+        if (n.get_function(&out->fns[m], mod, names_s[m]) != CUDA_SUCCESS) return nullptr;
+        if (n.func_set_attr(out->fns[m], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)out->smem_s) !=
             CUDA_SUCCESS)
             return nullptr;
     }
@@ -403,13 +416,15 @@ cudaError_t launch_spans_jit(const DevPsf& p, const Geom& g, const Epi& e, cudaS
     a.tend = e.tend;
     const int rows = g.y1 - g.y0;
     if (rows <= 0) return cudaSuccess;
-    const int TH = k->V * k->NTY;
+    const bool small = (long long)g.W * rows * g.batch <= JIT_SMALL_PX;
+    const int V = small ? 2 : k->V, NTY = small ? 4 : k->NTY, TH = V * NTY;
     const int m = e.mode == EPI_STORE ? 0 : e.mode == EPI_QUOT ? 1 : e.mode == EPI_UPDATE ? 2 : -1;
     if (m < 0) return cudaErrorInvalidValue;
     void* args[] = {&a};
-    const CUresult r = nvrtc().launch(k->fn[m], (unsigned)((g.W + 127) / 128), (unsigned)((rows + TH - 1) / TH),
-                                      (unsigned)g.batch, 32u * k->NTY, 1, 1, (unsigned)k->smem,
-                                      reinterpret_cast<CUstream>(st), args, nullptr);
+    const CUresult r = nvrtc().launch(small ? k->fns[m] : k->fn[m], (unsigned)((g.W + 127) / 128),
+                                      (unsigned)((rows + TH - 1) / TH), (unsigned)g.batch, 32u * NTY, 1, 1,
+                                      (unsigned)(small ? k->smem_s : k->smem), reinterpret_cast<CUstream>(st), args,
+                                      nullptr);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
 }
 
