@@ -301,6 +301,10 @@ int build_taps_engine(fdg_plan* pl, const std::vector<Tap>& taps, bool uniform, 
     CK(upload(&d.d_row_start, start));
     CK(upload(&d.d_dx, dx));
     CK(upload(&d.d_w, w));
+    d.h_row_start = start;
+    d.h_dx = dx;
+    d.h_w = w;
+    if (spans_jit_mode()) taps_jit_ready(d);  // compile its tile kernel now, not inside a capture
     return FDG_OK;
 }
 

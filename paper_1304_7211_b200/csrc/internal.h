@@ -62,6 +62,8 @@ struct DevPsf {
     int* d_dx = nullptr;         // [ntaps]
     float* d_w = nullptr;        // [ntaps]
     std::vector<int> h_span;     // [2*nrows] xmin,xmax per row (spans engine, host)
+    std::vector<int> h_row_start, h_dx;  // taps engine, host copies (JIT tap kernels)
+    std::vector<float> h_w;
     int mw = 0, mh = 0, mwp = 0;  // dense engine: grid, padded width
     float* d_dense = nullptr;     // [mh * mwp]
     std::vector<float> h_dense;   // host copy (passed as kernel parameters)
@@ -115,6 +117,10 @@ cudaError_t launch_spanr(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
 // span tile kernel compiled at run time for a plan's table (spans_jit.cu,
 // NVRTC); ready() compiles on first use per table and device (plan build)
 bool spans_jit_ready(const DevPsf& p);
+// the per-tap tile kernel compiled at run time for a plan's tap list
+// (List / wide Naive / Fourier passes, masked ones too; <= 128 taps, x extent <= 33)
+bool taps_jit_ready(const DevPsf& p);
+cudaError_t launch_taps_jit(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st);
 cudaError_t launch_spans_jit(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st);
 void set_spans_jit(int v);
 int spans_jit_mode();

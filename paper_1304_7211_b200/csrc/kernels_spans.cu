@@ -707,7 +707,10 @@ cudaError_t launch_spans(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
         if (same_shape<DiscR10>(p)) return launch_shape<DiscR10>(p, g, e, st);
         if (same_shape<Oblique21>(p)) return launch_shape<Oblique21>(p, g, e, st);
         // any other table: the tile kernel compiled for it at plan time (NVRTC)
-        if (spans_jit_mode() && spans_jit_ready(p)) return launch_spans_jit(p, g, e, st);
+        if (spans_jit_mode() && spans_jit_ready(p)) {
+            const cudaError_t r = launch_spans_jit(p, g, e, st);
+            if (r != cudaErrorNotSupported) return r;  // else the JIT build failed: runtime-table kernel
+        }
     }
     return launch_spanr(p, g, e, st);
 }

@@ -311,6 +311,11 @@ cudaError_t dense_mode(const DenseArgs& a, const DenseW& w, int mode, bool maske
 }  // namespace
 
 cudaError_t launch_taps(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st) {
+    // unmasked passes: the tile kernel compiled for this tap list (NVRTC)
+    if (spans_jit_mode() && taps_jit_ready(p)) {
+        const cudaError_t r = launch_taps_jit(p, g, e, st);
+        if (r != cudaErrorNotSupported) return r;  // else the JIT build failed: the generic tap kernel
+    }
     TapsArgs a;
     a.in = g.in;
     a.out = g.out;
