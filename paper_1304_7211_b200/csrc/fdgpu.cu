@@ -609,7 +609,7 @@ int enter(fdg_ctx* ctx, Entry& en) {
 }
 
 // engine options a captured graph depends on
-int options_key() { return fused_mode() * 16 + spans_mode(); }
+int options_key() { return fused_mode() * 16 + spans_mode() + 256 * spans_jit_mode(); }
 
 bool pageable(const void* p) {
     cudaPointerAttributes a;
