@@ -93,6 +93,28 @@ __device__ void spant(const JitArgs& a) {
     const int sb = x0 - E::HL;
     constexpr int NQ = TC / 4;
     const bool col_interior = sb >= 0 && sb + TC <= a.W;
+    // epilogue operand of this thread's V rows, loaded before the tile so its
+    // latency overlaps the tile load (the small-image launches are latency bound)
+    float4 pre[V];
+    {
+        const int xq = x0 + 4 * tx;
+#pragma unroll
+        for (int o = 0; o < V; ++o) {
+            pre[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int y = min(yt0 + ty * V + o, a.y1 - 1);
+            if ((MODE == 1 || MODE == 2) && xq < a.W) {
+                const long long idx = img + (long long)y * a.pitch + xq;
+                if (xq + 3 < a.W) {
+                    pre[o] = __ldg(reinterpret_cast<const float4*>(a.aux + idx));
+                } else {
+                    pre[o].x = a.aux[idx];
+                    if (xq + 1 < a.W) pre[o].y = a.aux[idx + 1];
+                    if (xq + 2 < a.W) pre[o].z = a.aux[idx + 2];
+                }
+            }
+        }
+    }
+
     for (int k = threadIdx.x; k < TR * NQ; k += 32 * NTY) {
         const int t = k / NQ, q = k - t * NQ;
         const int row = clampi(yt0 + SH::MINDY + t, a.ylo, a.yhi);
@@ -168,16 +190,7 @@ __device__ void spant(const JitArgs& a) {
             const int y = yo0 + o;
             if (y >= a.y1) break;
             const long long idx = img + (long long)y * a.pitch + xc;
-            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (MODE != 0) {
-                if (full_store) {
-                    x = __ldg(reinterpret_cast<const float4*>(a.aux + idx));
-                } else {
-                    x.x = a.aux[idx];
-                    if (xc + 1 < a.W) x.y = a.aux[idx + 1];
-                    if (xc + 2 < a.W) x.z = a.aux[idx + 2];
-                }
-            }
+            float4 x = pre[o];
             float4 vv = make_float4(acc[o].x * a.scale, acc[o].y * a.scale, acc[o].z * a.scale, acc[o].w * a.scale);
             if (!full_store) {
                 if (xc + 1 >= a.W) vv.y = x.y = 0.f;
@@ -301,6 +314,27 @@ __device__ void tapt(const JitArgs& a) {
     const float* src = a.in + img;
     const int cb = x0 + TP::MINDX;  // image column of tile column 0
     const int hgt = a.yhi - a.ylo + 1;
+    // epilogue operand of this thread's V rows, loaded before the tile so its
+    // latency overlaps the tile load (the small-image launches are latency bound)
+    float4 pre[V];
+    {
+        const int xq = x0 + 4 * tx;
+#pragma unroll
+        for (int o = 0; o < V; ++o) {
+            pre[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int y = min(yt0 + ty * V + o, a.y1 - 1);
+            if ((MODE == 1 || MODE == 2) && xq < a.W) {
+                const long long idx = img + (long long)y * a.pitch + xq;
+                if (xq + 3 < a.W) {
+                    pre[o] = __ldg(reinterpret_cast<const float4*>(a.aux + idx));
+                } else {
+                    pre[o].x = a.aux[idx];
+                    if (xq + 1 < a.W) pre[o].y = a.aux[idx + 1];
+                    if (xq + 2 < a.W) pre[o].z = a.aux[idx + 2];
+                }
+            }
+        }
+    }
     if (MODE >= 3) {  // thinned pass: tiles without an active output pixel keep their fallback
         int any = 0;
         const int xq = x0 + 4 * tx;
@@ -411,16 +445,7 @@ __device__ void tapt(const JitArgs& a) {
             const int y = yo0 + o;
             if (y >= a.y1) break;
             const long long idx = img + (long long)y * a.pitch + xc;
-            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (MODE != 0) {
-                if (full_store) {
-                    x = __ldg(reinterpret_cast<const float4*>(a.aux + idx));
-                } else {
-                    x.x = a.aux[idx];
-                    if (xc + 1 < a.W) x.y = a.aux[idx + 1];
-                    if (xc + 2 < a.W) x.z = a.aux[idx + 2];
-                }
-            }
+            float4 x = pre[o];
             float4 vv = acc[o];
             if (TP::UNI) vv = make_float4(vv.x * a.scale, vv.y * a.scale, vv.z * a.scale, vv.w * a.scale);
             if (!full_store) {
