@@ -343,6 +343,15 @@ int build_plan(fdg_ctx* ctx, const HostPsf& psf, int preference, std::unique_ptr
                 d.max_dy = r.min_dy + r.my - 1;
                 d.uniform = 1;
                 d.scale = (float)scale;
+                // the same box as a span table (every row [min_dx, max_dx]):
+                // small images run it through the compiled span tile kernel,
+                // the row-streaming box engine being latency bound there
+                d.nrows = r.my;
+                d.h_span.clear();
+                for (int y = 0; y < r.my; ++y) {
+                    d.h_span.push_back(d.min_dx);
+                    d.h_span.push_back(d.max_dx);
+                }
             } else {
                 std::vector<Tap> t;
                 for (int y = 0; y < r.my; ++y)
@@ -451,6 +460,11 @@ int run_pass(fdg_ctx* ctx, const fdg_plan* pl, const Geom& g, const Epi& e, cuda
     switch (d.engine) {
         case ENG_RECT:
             if (masked) return set_err(FDG_EINVAL, "operator does not support masked evaluation");
+            if (!g.wrap && (long long)g.W * (g.y1 - g.y0) * g.batch <= (512 << 10) && spans_jit_mode() &&
+                spans_jit_ready(d)) {
+                r = launch_spans_jit(d, g, e, st);
+                if (r != cudaErrorNotSupported) break;
+            }
             r = launch_rect(d, g, e, st);
             break;
         case ENG_SPANS:
