@@ -163,7 +163,9 @@ int fdg_conv_apply_device(fdg_plan* plan, const float* d_in, float* d_out, int w
 /* rlDeconvolve, rl.hpp:140-179.  trace: nullable, cfg->iterations records;
  * seconds = per-iteration device time (%globaltimer stamps written by each
  * iteration's last kernel, so graph-replayed loops report real per-iteration
- * times) */
+ * times).  The input check of rl.hpp:78-83 runs on the device and its
+ * verdict returns with the trace (one synchronisation per call): on any
+ * error the contents of u_out are unspecified. */
 int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg,
                       const float* f, int width, int height, float* u_out, fdg_rl_record* trace);
 /* rlDeconvolveSelective, rl.hpp:187-257.  thin_start: deactivation is held

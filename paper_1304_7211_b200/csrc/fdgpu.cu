@@ -147,6 +147,7 @@ struct fdg_ctx {
     DevBuf<unsigned> tr_max;
     DevBuf<int> tr_nan;
     DevBuf<unsigned long long> tr_inact, first_bad, tr_time;
+    unsigned long long* h_bad = nullptr;  // page-locked copy of first_bad (deferred validation)
     // masked dense passes: compacted active-block lists per 64x64 tile
     DevBuf<int> tile_blocks, tile_count;
     // rlDeconvolve on host buffers keeps the last call's solver (plans + the
@@ -205,6 +206,7 @@ struct fdg_solver {
     DevBuf<unsigned long long> tstamp;
     DevBuf<unsigned long long> tdur;  // row-resident runs: per-iteration durations summed over CTAs
     bool last_rowres = false;         // engine of the last run (trace seconds)
+    void* h_trace = nullptr;          // page-locked landing area of the trace copies
     // CUDA graph of one full fdg_solver_run (replayed while the arguments and
     // the engine options it was captured under match)
     cudaGraphExec_t gexec = nullptr;
@@ -225,6 +227,7 @@ struct fdg_solver {
         if (ev_in) cudaEventDestroy(ev_in);
         if (ev_out) cudaEventDestroy(ev_out);
         if (gstream) cudaStreamDestroy(gstream);
+        if (h_trace) cudaFreeHost(h_trace);
         fwd.reset();
         adj.reset();
         maxchange.release();
@@ -246,6 +249,7 @@ fdg_ctx::~fdg_ctx() {
     if (own_stream) cudaStreamDestroy(stream);
     a.release(), b.release(), c.release(), d.release(), m.release();
     tr_max.release(), tr_nan.release(), tr_inact.release(), first_bad.release(), tr_time.release();
+    if (h_bad) cudaFreeHost(h_bad);
     tile_blocks.release(), tile_count.release();
 }
 
@@ -1340,20 +1344,26 @@ int solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long
 int solver_trace(fdg_solver* s, int n, std::vector<float>* mc, std::vector<int>* nf, std::vector<double>* sec) {
     cudaStream_t st = s->ctx->stream;
     n = std::min(n, s->ntrace);
-    std::vector<unsigned> m(n);
-    std::vector<unsigned long long> ts(n + 1), dur;
-    nf->assign(n, 0);
-    CK(cudaMemcpyAsync(m.data(), s->maxchange.p, sizeof(unsigned) * n, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(nf->data(), s->nanflag.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(ts.data(), s->tstamp.p, sizeof(unsigned long long) * (n + 1), cudaMemcpyDeviceToHost, st));
-    if (s->last_rowres) {
-        dur.resize(n);
-        CK(cudaMemcpyAsync(dur.data(), s->tdur.p, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, st));
-    }
+    // page-locked landing area (async DMA, no pageable staging): ts[n + 1], dur[n], mc[n], nf[n]
+    const size_t bytes = sizeof(unsigned long long) * (2 * (size_t)s->ntrace + 1) + 2 * sizeof(unsigned) * s->ntrace;
+    if (!s->h_trace) CK(cudaHostAlloc(&s->h_trace, bytes, cudaHostAllocDefault));
+    unsigned long long* ts = reinterpret_cast<unsigned long long*>(s->h_trace);
+    unsigned long long* du = ts + s->ntrace + 1;
+    unsigned* m = reinterpret_cast<unsigned*>(du + s->ntrace);
+    int* f = reinterpret_cast<int*>(m + s->ntrace);
+    CK(cudaMemcpyAsync(m, s->maxchange.p, sizeof(unsigned) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(f, s->nanflag.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ts, s->tstamp.p, sizeof(unsigned long long) * (n + 1), cudaMemcpyDeviceToHost, st));
+    if (s->last_rowres)
+        CK(cudaMemcpyAsync(du, s->tdur.p, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     mc->resize(n);
+    nf->assign(f, f + n);
     for (int k = 0; k < n; ++k) std::memcpy(&(*mc)[k], &m[k], sizeof(float));
-    *sec = trace_seconds(ts, dur, n);
+    const std::vector<unsigned long long> tsv(ts, ts + n + 1);
+    std::vector<unsigned long long> duv;
+    if (s->last_rowres) duv.assign(du, du + n);
+    *sec = trace_seconds(tsv, duv, n);
     return FDG_OK;
 }
 
@@ -1456,9 +1466,16 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     float *df = ctx->a.p, *du = ctx->b.p, *dq = ctx->c.p;
     pt.mark("alloc");
     if ((st = h2d(ctx->stg, df, pitch, f, W, H, s))) return st;
-    if ((st = validate_device(ctx, df, W, H, pitch, "rlDeconvolve"))) return st;
+    if (!sv && (st = validate_device(ctx, df, W, H, pitch, "rlDeconvolve"))) return st;
     pt.mark("h2d+validate");
     if (sv) {
+        // rl.hpp:78-83 checked on the device without a round trip of its own:
+        // the verdict travels back with the trace and is looked at first
+        CK(ctx->first_bad.ensure(2));
+        if (!ctx->h_bad) CK(cudaHostAlloc(&ctx->h_bad, 2 * sizeof(unsigned long long), cudaHostAllocDefault));
+        CK(launch_validate(df, W, H, pitch, ctx->first_bad.p, s));
+        ctx->launches += 1;
+        CK(cudaMemcpyAsync(ctx->h_bad, ctx->first_bad.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         if ((st = solver_reset_trace(sv))) return st;
         if ((st = solver_run(sv, df, du, pitch, 0, iters))) return st;
         prefault(u_out, (size_t)W * H * sizeof(float));
@@ -1472,6 +1489,9 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
         std::vector<double> sec;
         if ((st = solver_trace(sv, iters, &mc, &nf, &sec))) return st;  // synchronises the stream
         pt.mark("d2h");
+        const unsigned long long nf0 = ctx->h_bad[0], neg0 = ctx->h_bad[1];
+        if (nf0 != ~0ull && nf0 <= neg0) return set_err(FDG_EINVAL, "rlDeconvolve: input image has non-finite pixels");
+        if (neg0 != ~0ull) return set_err(FDG_EINVAL, "rlDeconvolve: input image must be nonnegative");
         for (int k = 0; k < iters; ++k) {
             if (nf[k]) return set_err(FDG_ENAN, "rlDeconvolve: NaN in iterate at iteration " + std::to_string(k + 1));
             // per-iteration seconds from the device stamps of the replayed graph

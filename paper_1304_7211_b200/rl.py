@@ -101,9 +101,17 @@ def _validate(a: np.ndarray, cfg: RlConfig, where: str):
     _lib.validate_image(a, where)
 
 
+_REC_DTYPE = np.dtype([("iteration", "<i4"), ("_pad", "<i4"), ("inactive", "<f8"), ("maxc", "<f8"),
+                       ("sec", "<f8")])
+
+
 def _trace(recs, n) -> RlTrace:
-    return RlTrace([RlIterationRecord(recs[i].iteration, recs[i].inactive_fraction, recs[i].max_abs_change,
-                                      recs[i].seconds) for i in range(n)])
+    if n <= 0:
+        return RlTrace([])
+    # one numpy view of the C records (per-field ctypes access costs ~1 us each)
+    a = np.frombuffer(recs, dtype=_REC_DTYPE, count=n)
+    return RlTrace([RlIterationRecord(int(i), float(f), float(m), float(t))
+                    for i, f, m, t in zip(a["iteration"], a["inactive"], a["maxc"], a["sec"])])
 
 
 def _out(a, u32):
