@@ -168,6 +168,15 @@ int fdg_conv_apply_device(fdg_plan* plan, const float* d_in, float* d_out, int w
  * error the contents of u_out are unspecified. */
 int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg,
                       const float* f, int width, int height, float* u_out, fdg_rl_record* trace);
+/* rlDeconvolve over `batch` independent width x height images stored one
+ * after another (f, u_out: batch * width * height floats).  One solver runs
+ * the images in chunks; with page-locked host buffers the upload of the next
+ * chunk and the download of the previous one overlap the iterations of the
+ * current chunk (copy engines vs SMs).  trace (nullable, iterations
+ * records): max|du| over the batch, seconds summed over the chunks.  Same
+ * errors as fdg_rl_deconvolve (any image). */
+int fdg_rl_deconvolve_batch(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg, const float* f,
+                            int width, int height, int batch, float* u_out, fdg_rl_record* trace);
 /* rlDeconvolveSelective, rl.hpp:187-257.  thin_start: deactivation is held
  * off for 0-based k < thin_start (0 = the reference).  mask_replay
  * (nullable, iterations*width*height bytes) replaces the device's own

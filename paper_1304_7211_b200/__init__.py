@@ -11,7 +11,7 @@ from .psf import (DensePsf, UniformConvexPsf, SparsePsf, makeLinePsf, makeBoxPsf
 from .pgm import PgmParseError, readPgm, writePgm, readPgmFile, writePgmFile, snrDb
 from .convolve import (OperatorKind, operatorName, operatorKindFromName, supportsMasking,
                        operatorAcceptsPsf, dispatch, ConvCounters, ConvPlan, convolve, maskedConvolve)
-from .rl import (RlConfig, RlIterationRecord, RlTrace, RlResult, rlDeconvolve, rlDeconvolveSelective,
+from .rl import (RlConfig, RlIterationRecord, RlTrace, RlResult, rlDeconvolve, rlDeconvolveBatch, rlDeconvolveSelective,
                  rlStep, blurImage, BoundaryMode, RlSolver)
 from ._lib import FdgError, lib_path
 

@@ -124,6 +124,8 @@ def lib():
             "fdg_rl_deconvolve_selective": (C.c_int, [vp, D, C.POINTER(RlConfigC), C.c_double, C.c_int,
                                                       C.c_int, u8p, u8p, fp, C.c_int, C.c_int, fp,
                                                       C.POINTER(RlRecordC)]),
+            "fdg_rl_deconvolve_batch": (C.c_int, [vp, D, C.POINTER(RlConfigC), fp, C.c_int, C.c_int, C.c_int, fp,
+                                                  C.POINTER(RlRecordC)]),
             "fdg_rl_step": (C.c_int, [vp, D, C.POINTER(RlConfigC), fp, fp, C.c_int, C.c_int, fp, dp]),
             "fdg_solver_create": (C.c_int, [vp, D, C.POINTER(RlConfigC), C.c_int, C.c_int, C.c_int,
                                             C.POINTER(vp)]),

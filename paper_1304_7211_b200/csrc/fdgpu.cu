@@ -128,6 +128,8 @@ struct DevScope {
 namespace {
 struct SelCache;
 void sel_destroy(SelCache* c);
+struct BatchCache;
+void batch_destroy(BatchCache* c);
 }  // namespace
 
 struct fdg_ctx {
@@ -157,6 +159,8 @@ struct fdg_ctx {
     // rlDeconvolveSelective likewise keeps its buffers and the captured
     // graph of the whole thinned loop (calls without mask replay / record)
     SelCache* sel = nullptr;
+    // fdg_rl_deconvolve_batch: its chunked solver, planes and copy streams
+    BatchCache* batch = nullptr;
     ~fdg_ctx();
 };
 
@@ -207,6 +211,7 @@ struct fdg_solver {
     DevBuf<unsigned long long> tdur;  // row-resident runs: per-iteration durations summed over CTAs
     bool last_rowres = false;         // engine of the last run (trace seconds)
     void* h_trace = nullptr;          // page-locked landing area of the trace copies
+    bool graph_off = false;           // launch directly (batched chunks change pointers every run)
     // CUDA graph of one full fdg_solver_run (replayed while the arguments and
     // the engine options it was captured under match)
     cudaGraphExec_t gexec = nullptr;
@@ -246,6 +251,7 @@ fdg_ctx::~fdg_ctx() {
     if (stream) cudaStreamSynchronize(stream);
     fdg_solver_destroy(rl_solver);
     sel_destroy(sel);
+    batch_destroy(batch);
     if (own_stream) cudaStreamDestroy(stream);
     a.release(), b.release(), c.release(), d.release(), m.release();
     tr_max.release(), tr_nan.release(), tr_inact.release(), first_bad.release(), tr_time.release();
@@ -1235,7 +1241,8 @@ int solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long
     // Replay the captured graph when the arguments and options are unchanged:
     // the whole run (start stamp + every iteration's launches) is one
     // cudaGraphLaunch.
-    static const bool no_graph = getenv("FDG_NO_GRAPH") != nullptr;
+    static const bool no_graph_env = getenv("FDG_NO_GRAPH") != nullptr;
+    const bool no_graph = no_graph_env || s->graph_off;
     if (!no_graph && !s->gstream) {
         CK(cudaStreamCreateWithFlags(&s->gstream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming));
@@ -2028,6 +2035,173 @@ int fdg_mask_compact(fdg_ctx* ctx, const uint8_t* active, int W, int H, int64_t*
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------- batched RL
+// fdg_rl_deconvolve_batch: `batch` independent images of one size through
+// one solver, in chunks, the H2D of chunk c + 1 and the D2H of chunk c - 1
+// overlapping the iterations of chunk c (copy engines vs SMs; page-locked
+// host buffers; pageable ones fall back to one chunk at a time).
+namespace {
+struct BatchCache {
+    std::string key;
+    std::unique_ptr<fdg_solver> sv;
+    int W = 0, H = 0, chunk = 0, pitch = 0;
+    DevBuf<float> f, u;
+    DevBuf<unsigned long long> bad;  // per chunk: first non-finite / negative index
+    DevBuf<unsigned> tmc;            // per chunk x iteration: max|du| bits, NaN flag
+    DevBuf<int> tnf;
+    DevBuf<unsigned long long> tts;  // per chunk: iteration end stamps (iters + 1)
+    void* host = nullptr;            // page-locked landing area of the verdicts and traces
+    cudaStream_t cin = nullptr, cout_ = nullptr;
+    std::vector<cudaEvent_t> ev;  // per chunk: in, done
+    int device = 0;
+    ~BatchCache() {
+        DevScope ds;
+        ds.enter(device);
+        if (cin) cudaStreamSynchronize(cin), cudaStreamDestroy(cin);
+        if (cout_) cudaStreamSynchronize(cout_), cudaStreamDestroy(cout_);
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+        if (host) cudaFreeHost(host);
+        sv.reset();
+    }
+};
+void batch_destroy(BatchCache* c) { delete c; }
+}  // namespace
+
+extern "C" int fdg_rl_deconvolve_batch(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg,
+                                       const float* f, int W, int H, int batch, float* u_out, fdg_rl_record* trace) {
+    int st = validate_cfg(f, W, H, cfg, "rlDeconvolve");
+    if (st) return st;
+    if (batch < 1 || !u_out) return set_err(FDG_EINVAL, "rlDeconvolve: empty batch");
+    if (!ctx) return set_err(FDG_ECUDA, "no CUDA context (no device available; the B200 path has no CPU fallback)");
+    Entry en;
+    if ((st = enter(ctx, en))) return st;
+    const int iters = cfg->iterations;
+    const size_t px = (size_t)W * H;
+    // ~8 chunks (>= 2 when the batch allows, >= 16 Mpx each): long enough
+    // launches, short enough pipeline fill / drain (FDG_BATCH_CHUNK overrides)
+    static const int chunk_env = getenv("FDG_BATCH_CHUNK") ? atoi(getenv("FDG_BATCH_CHUNK")) : 0;
+    int chunk = std::max(1, std::min((batch + 1) / 2, std::max((batch + 7) / 8, (int)((16u << 20) / px))));
+    if (chunk_env > 0) chunk = std::min(batch, chunk_env);
+    const int nchunk = (batch + chunk - 1) / chunk;
+    std::string key = rl_cache_key(desc, cfg, W, H) + "#" + std::to_string(chunk) + "#" + std::to_string(batch);
+    BatchCache* bc = ctx->batch;
+    if (!bc || bc->key != key) {
+        batch_destroy(ctx->batch);
+        ctx->batch = nullptr;
+        auto n = std::make_unique<BatchCache>();
+        n->device = ctx->device;
+        if ((st = solver_create(ctx, desc, cfg, W, H, chunk, &n->sv))) return st;
+        n->W = W;
+        n->H = H;
+        n->chunk = chunk;
+        n->pitch = pitch_for(W);
+        CK(n->f.ensure((size_t)n->pitch * H * batch));
+        CK(n->u.ensure((size_t)n->pitch * H * batch));
+        CK(n->bad.ensure(2 * (size_t)nchunk));
+        const size_t ni = std::max(iters, 1);
+        CK(n->tmc.ensure(ni * nchunk));
+        CK(n->tnf.ensure(ni * nchunk));
+        CK(n->tts.ensure((ni + 1) * nchunk));
+        CK(cudaHostAlloc(&n->host, sizeof(unsigned long long) * (2 * nchunk + (ni + 1) * nchunk) +
+                                       2 * sizeof(unsigned) * ni * nchunk,
+                         cudaHostAllocDefault));
+        CK(cudaStreamCreateWithFlags(&n->cin, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&n->cout_, cudaStreamNonBlocking));
+        n->ev.resize(2 * nchunk);
+        for (cudaEvent_t& e : n->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        n->key = std::move(key);
+        bc = ctx->batch = n.release();
+    }
+    const int pitch = bc->pitch;
+    const size_t stride = (size_t)pitch * H;
+    cudaStream_t comp = ctx->stream;
+    const bool pinned = !pageable(f) && !pageable(u_out);
+    const size_t ni = std::max(iters, 1);
+    const size_t row = (size_t)W * 4;
+    if (pinned) {  // every upload queued up front on the copy stream (after the caller's prior work)
+        CK(cudaEventRecord(bc->ev[0], comp));
+        CK(cudaStreamWaitEvent(bc->cin, bc->ev[0], 0));
+        for (int c = 0; c < nchunk; ++c) {
+            const int i0 = c * chunk, nb = std::min(chunk, batch - i0);
+            CK(cudaMemcpy2DAsync(bc->f.p + stride * i0, (size_t)pitch * 4, f + px * i0, row, row, (size_t)H * nb,
+                                 cudaMemcpyHostToDevice, bc->cin));
+            CK(cudaEventRecord(bc->ev[2 * c], bc->cin));
+        }
+    }
+    for (int c = 0; c < nchunk; ++c) {
+        const int i0 = c * chunk, nb = std::min(chunk, batch - i0);
+        float* df = bc->f.p + stride * i0;
+        float* du = bc->u.p + stride * i0;
+        if (pinned) {
+            CK(cudaStreamWaitEvent(comp, bc->ev[2 * c], 0));
+        } else if ((st = h2d(ctx->stg, df, pitch, f + px * i0, W, H * nb, comp))) {
+            return st;
+        }
+        // rl.hpp:78-83 per chunk on the device; verdicts read at the end
+        CK(launch_validate(df, W, H * nb, pitch, bc->bad.p + 2 * c, comp));
+        ctx->launches += 1;
+        fdg_solver* sv = bc->sv.get();
+        if (nb != sv->batch) {  // the last, shorter chunk
+            sv->batch = nb;
+        }
+        if ((st = solver_reset_trace(sv))) return st;
+        sv->graph_off = true;  // a new pointer pair every chunk: launch, do not capture
+        if ((st = solver_run(sv, df, du, pitch, (long long)stride, iters))) return st;
+        sv->batch = chunk;
+        if (iters > 0) {  // park this chunk's trace slots (reset by the next chunk) on the device
+            CK(cudaMemcpyAsync(bc->tmc.p + ni * c, sv->maxchange.p, sizeof(unsigned) * iters,
+                               cudaMemcpyDeviceToDevice, comp));
+            CK(cudaMemcpyAsync(bc->tnf.p + ni * c, sv->nanflag.p, sizeof(int) * iters, cudaMemcpyDeviceToDevice,
+                               comp));
+            CK(cudaMemcpyAsync(bc->tts.p + (ni + 1) * c, sv->tstamp.p, sizeof(unsigned long long) * (iters + 1),
+                               cudaMemcpyDeviceToDevice, comp));
+        }
+        if (pinned) {
+            CK(cudaEventRecord(bc->ev[2 * c + 1], comp));
+            CK(cudaStreamWaitEvent(bc->cout_, bc->ev[2 * c + 1], 0));
+            CK(cudaMemcpy2DAsync(u_out + px * i0, row, du, (size_t)pitch * 4, row, (size_t)H * nb,
+                                 cudaMemcpyDeviceToHost, bc->cout_));
+        } else if ((st = d2h(ctx->stg, u_out + px * i0, du, pitch, W, H * nb, comp))) {
+            return st;
+        }
+    }
+    // one trip back: every chunk's input verdict and trace
+    unsigned long long* hbad = static_cast<unsigned long long*>(bc->host);
+    unsigned long long* hts = hbad + 2 * nchunk;
+    unsigned* hmc = reinterpret_cast<unsigned*>(hts + (ni + 1) * nchunk);
+    int* hnf = reinterpret_cast<int*>(hmc + ni * nchunk);
+    CK(cudaMemcpyAsync(hbad, bc->bad.p, sizeof(unsigned long long) * 2 * nchunk, cudaMemcpyDeviceToHost, comp));
+    if (iters > 0) {
+        CK(cudaMemcpyAsync(hts, bc->tts.p, sizeof(unsigned long long) * (ni + 1) * nchunk, cudaMemcpyDeviceToHost,
+                           comp));
+        CK(cudaMemcpyAsync(hmc, bc->tmc.p, sizeof(unsigned) * ni * nchunk, cudaMemcpyDeviceToHost, comp));
+        CK(cudaMemcpyAsync(hnf, bc->tnf.p, sizeof(int) * ni * nchunk, cudaMemcpyDeviceToHost, comp));
+    }
+    if (pinned) CK(cudaStreamSynchronize(bc->cout_));
+    CK(cudaStreamSynchronize(comp));
+    for (int c = 0; c < nchunk; ++c) {
+        const unsigned long long nf0 = hbad[2 * c], neg0 = hbad[2 * c + 1];
+        if (nf0 != ~0ull && nf0 <= neg0) return set_err(FDG_EINVAL, "rlDeconvolve: input image has non-finite pixels");
+        if (neg0 != ~0ull) return set_err(FDG_EINVAL, "rlDeconvolve: input image must be nonnegative");
+    }
+    for (int k = 0; k < iters; ++k) {
+        float mmax = 0.f;
+        int nan = 0;
+        double sec = 0.0;
+        for (int c = 0; c < nchunk; ++c) {
+            float m;
+            std::memcpy(&m, &hmc[ni * c + k], sizeof m);
+            mmax = std::max(mmax, m);
+            nan |= hnf[ni * c + k];
+            const unsigned long long* t = hts + (ni + 1) * c;
+            if (t[k] && t[k + 1] > t[k]) sec += (double)(t[k + 1] - t[k]) * 1e-9;
+        }
+        if (nan) return set_err(FDG_ENAN, "rlDeconvolve: NaN in iterate at iteration " + std::to_string(k + 1));
+        if (trace) trace[k] = {k + 1, 0.0, (double)mmax, sec};
+    }
+    return FDG_OK;
+}
 
 // row-strip sharded RL (fdg_shard_*): uses the internals above
 #include "shard.cuh"

@@ -141,6 +141,32 @@ def rlDeconvolve(f, h, cfg: RlConfig = RlConfig(), ctx: Optional[Context] = None
     return RlResult(_out(a, u), _trace(recs, n))
 
 
+def rlDeconvolveBatch(fs, h, cfg: RlConfig = RlConfig(), ctx: Optional[Context] = None,
+                      out: Optional[np.ndarray] = None) -> RlResult:
+    """rlDeconvolve (rl.hpp:140-179) over a (batch, H, W) stack of independent
+    images in one call (fdg_rl_deconvolve_batch): with page-locked input /
+    output the uploads and downloads of neighbouring chunks overlap the
+    iterations.  trace: per iteration, max|du| over the batch."""
+    a = np.asarray(fs)
+    if a.ndim != 3 or a.size == 0:
+        raise _lib.FdgInvalidArgument("rlDeconvolve: empty input image")
+    _validate(a, cfg, "rlDeconvolve")
+    src = f32(a)
+    b, hh, w = src.shape
+    if out is not None:
+        if out.dtype != np.float32 or out.shape != src.shape or not out.flags.c_contiguous:
+            raise _lib.FdgInvalidArgument("rlDeconvolve: out must be a C-contiguous float32 array of the batch's shape")
+        u = out
+    else:
+        u = np.empty_like(src)
+    n = max(cfg.iterations, 0)
+    recs = (RlRecordC * max(n, 1))()
+    c = cfg.c()
+    check(lib().fdg_rl_deconvolve_batch(Context.handle_or_null(ctx), Desc(h).ref, C.byref(c), fptr(src), w, hh, b,
+                                        fptr(u), recs))
+    return RlResult(_out(a, u), _trace(recs, n))
+
+
 def rlDeconvolveSelective(f, h, cfg: RlConfig, threshold: float, period: int = 10, thin_start: int = 0,
                           mask_replay: Optional[np.ndarray] = None, record_masks: bool = False,
                           ctx: Optional[Context] = None) -> RlResult:
