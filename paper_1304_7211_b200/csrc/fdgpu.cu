@@ -363,6 +363,27 @@ int build_plan(fdg_ctx* ctx, const HostPsf& psf, int preference, std::unique_ptr
                     d.h_span.push_back(d.max_dx);
                 }
             } else {
+                // wider than the box engine: the box as a span table (every row
+                // [min_dx, max_dx]; compiled tile kernel or runtime table), else taps
+                d.min_dx = r.min_dx;
+                d.max_dx = r.min_dx + r.mx - 1;
+                d.min_dy = r.min_dy;
+                d.max_dy = r.min_dy + r.my - 1;
+                d.nrows = r.my;
+                d.h_span.clear();
+                for (int y = 0; y < r.my; ++y) {
+                    d.h_span.push_back(d.min_dx);
+                    d.h_span.push_back(d.max_dx);
+                }
+                if (spans_supported(d)) {
+                    d.engine = ENG_SPANS;
+                    d.uniform = 1;
+                    d.scale = (float)scale;
+                    if (spans_jit_mode()) spans_jit_ready(d);
+                    break;
+                }
+                d.h_span.clear();
+                d.nrows = 0;
                 std::vector<Tap> t;
                 for (int y = 0; y < r.my; ++y)
                     for (int x = 0; x < r.mx; ++x) t.push_back({r.min_dx + x, r.min_dy + y, scale});

@@ -118,7 +118,7 @@ cudaError_t launch_spanr(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
 // NVRTC); ready() compiles on first use per table and device (plan build)
 bool spans_jit_ready(const DevPsf& p);
 // the per-tap tile kernel compiled at run time for a plan's tap list
-// (List / wide Naive / Fourier passes, masked ones too; <= 128 taps, x extent <= 33)
+// (List / wide Naive / Fourier passes, masked ones too; <= 128 taps, x extent <= 65)
 bool taps_jit_ready(const DevPsf& p);
 cudaError_t launch_taps_jit(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st);
 cudaError_t launch_spans_jit(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st);

@@ -682,7 +682,7 @@ JitKernel* taps_get(const DevPsf& p) {
         (int)p.h_dx.size() != p.ntaps || (int)p.h_row_start.size() != p.nrows + 1)
         return nullptr;
     const int nwx = p.max_dx - p.min_dx + 1;
-    if (nwx > 33) return nullptr;
+    if (nwx > 65) return nullptr;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
     char buf[64];
