@@ -153,7 +153,7 @@ cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float
                           int batch, long long bstride, int iters, float eps, int clamp, unsigned* maxchange,
                           int* nanflag, unsigned long long* tend, unsigned long long* tbegin, unsigned long long* tdur,
                           cudaStream_t st);
-// Whole RL iteration in one pass for the centred 15x15 box (kernels_fused.cu):
+// Whole RL iteration in one pass for centred 9x9 / 15x15 / 17x17 boxes (kernels_fused.cu):
 // u_out = max(box*(f / max(box(u_in), eps)) * u_in, 0); u_in != u_out.
 bool fused_supported(int mx, int my, int min_dx, int min_dy);
 void set_fused_mode(int v);
@@ -171,7 +171,7 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
                          int yhi, int batch, long long bstride, float scale, float eps, int clamp,
                          unsigned* maxchange, int* nanflag, unsigned long long* tend, cudaStream_t st,
                          int halo_in = 0, int halo_out = 0, int pitch_h = 0, long long bstride_h = 0,
-                         int y2 = 0, int y3 = 0, int balanced = 1);
+                         int y2 = 0, int y3 = 0, int balanced = 1, int rx = 7);
 // The boundary bands of a row strip for the fused iteration (kernels_band.cu):
 // output rows [y0, y1) and [y2, y3) computed in place per 16 x 16 tile (no
 // row streaming), small enough to run next to the fused interior launch.

@@ -1,6 +1,7 @@
 // kernels_fused.cu -- one launch per Richardson-Lucy iteration for centred
-// separable boxes (Box2d*, config 4): both convolutions, the quotient and the
-// multiplicative update fused, q never leaving the SM.
+// square boxes 9 x 9 / 15 x 15 / 17 x 17 (Box2d*, config 4 = 15 x 15): both
+// convolutions, the quotient and the multiplicative update fused, q never
+// leaving the SM.
 //
 //   u_out = max( box*( f / max(box(u_in), eps) ) * u_in, 0 )
 //
@@ -125,6 +126,36 @@ __device__ __forceinline__ float4 hsum15x4(const float* seg, int chunk) {
     return cat4(o01, o23);
 }
 
+// (2 RX + 1)-wide window sums of 4 consecutive columns for any radius
+// RX <= 8: window e covers v[OFF + e .. OFF + e + 2 RX] of the chunks
+// starting at `chunk` (OFF = 8 - RX); additions only, the shared middle
+// v[OFF + 3 .. OFF + 2 RX] formed once.  RX = 7 takes hsum15x4.
+template <int RX>
+__device__ __forceinline__ float4 hsumx4(const float* seg, int chunk) {
+    if constexpr (RX == 7) {
+        return hsum15x4(seg, chunk);
+    } else {
+        constexpr int OFF = 8 - RX, LAST = OFF + 3 + 2 * RX;
+        constexpr int C0 = OFF / 4, C1 = LAST / 4;
+        float v[4 * (C1 + 1)];
+        const float4* p = reinterpret_cast<const float4*>(seg) + chunk;
+#pragma unroll
+        for (int c = C0; c <= C1; ++c) {
+            const float4 q = p[c];
+            v[4 * c] = q.x;
+            v[4 * c + 1] = q.y;
+            v[4 * c + 2] = q.z;
+            v[4 * c + 3] = q.w;
+        }
+        float mid = 0.f;
+#pragma unroll
+        for (int k = 3; k <= 2 * RX; ++k) mid += v[OFF + k];
+        const float a = v[OFF + 1] + v[OFF + 2];
+        const float b = v[OFF + 2 * RX + 1] + v[OFF + 2 * RX + 2];
+        return make_float4(v[OFF] + a + mid, a + mid + v[OFF + 2 * RX + 1], v[OFF + 2] + mid + b,
+                           mid + b + v[OFF + 2 * RX + 3]);
+    }
+}
 
 // max that propagates NaN (the reference's clamp `value < 0 ? 0 : value`
 // keeps a NaN, and a NaN anywhere must reach the per-iteration check)
@@ -179,7 +210,7 @@ template <int RX, int RY, int NT, int R, int S, int QR, int PD, bool HINT>
 __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     using G = FG<RX, RY, NT>;
     static_assert(R == 2, "stage logic assumes two rows per stage");
-    static_assert(G::MX == 15 && G::OFF == 1, "hsum15x4 reads 5 chunks, window at offset 1");
+    static_assert(G::OFF == 8 - RX, "window offset inside its chunk");
     constexpr int SS = S / R;
     constexpr int LAG = SS / 2;  // edge CTAs: the producer readies stage st - LAG
     constexpr int MY = G::MY;
@@ -383,7 +414,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
                 constexpr int ODD = decltype(odd)::value;
                 const bool par = ST ? ODD : (i & 1);
                 if (!par) mbar_wait(&gate[s], phase);
-                float4 h = hsum15x4(uring + (size_t)(s * R + par) * G::USEG, chunk);
+                float4 h = hsumx4<RX>(uring + (size_t)(s * R + par) * G::USEG, chunk);
                 if (par || (!ST && i == steps - 1)) {  // this thread is done with the stage's u rows
                     mbar_arrive(&empty[s]);
                     if (++s == SS) {
@@ -429,8 +460,8 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
                         // flight, then both q rows handed to the B warps
                         mbar_wait(&gate[s], phase);
                         const float* us = uring + (size_t)(s * R) * G::USEG;
-                        float4 h0 = hsum15x4(us, chunk);
-                        float4 h1 = hsum15x4(us + G::USEG, chunk);
+                        float4 h0 = hsumx4<RX>(us, chunk);
+                        float4 h1 = hsumx4<RX>(us + G::USEG, chunk);
                         mbar_arrive(&empty[s]);
                         if (++s == SS) {
                             s = 0;
@@ -528,7 +559,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         };
         auto take = [&](int r) {  // H2 of q row r (waits for the A warps, frees the slot)
             mbar_wait_sleep(&qfull[r & (QR - 1)], (r / QR) & 1, FDG_QSLEEP);
-            const float4 h = hsum15x4(qrow_ptr(r), tb);
+            const float4 h = hsumx4<RX>(qrow_ptr(r), tb);
             mbar_arrive(&qempty[r & (QR - 1)]);
             return h;
         };
@@ -768,8 +799,10 @@ std::atomic<int> g_fused{getenv("FDG_FUSED") ? atoi(getenv("FDG_FUSED")) : 1};
 void set_fused_mode(int v) { g_fused.store(v); }
 int fused_mode() { return g_fused.load(); }
 
+// centred square boxes 9 x 9, 15 x 15 (config 4) and 17 x 17
 bool fused_supported(int mx, int my, int min_dx, int min_dy) {
-    return g_fused.load() == 1 && mx == 15 && my == 15 && min_dx == -7 && min_dy == -7;
+    return g_fused.load() == 1 && mx == my && (mx == 9 || mx == 15 || mx == 17) && min_dx == -(mx / 2) &&
+           min_dy == -(my / 2);
 }
 
 int fused_halo_left() { return FUSED_HALO_L; }
@@ -787,7 +820,7 @@ cudaError_t launch_pad_halo(const float* src, int pitch_src, long long bs_src, f
 cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int y0, int y1, int ylo,
                          int yhi, int batch, long long bstride, float scale, float eps, int clamp, unsigned* maxchange, int* nanflag,
                          unsigned long long* tend, cudaStream_t st, int halo_in, int halo_out, int pitch_h,
-                         long long bstride_h, int y2, int y3, int balanced) {
+                         long long bstride_h, int y2, int y3, int balanced, int rx) {
     FusedArgs a;
     a.lin_len = balanced ? 0 : -1;
     a.y2 = y2;
@@ -818,6 +851,8 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
     a.nanflag = nanflag;
     a.tend = tend;
     static const int variant = getenv("FDG_FUSED_V") ? atoi(getenv("FDG_FUSED_V")) : 0;
+    if (rx == 4) return launch_t<4, 4, 128, 2, 12, 8, 2, true>(a, st);  // 9 x 9
+    if (rx == 8) return launch_t<8, 8, 128, 2, 12, 8, 2, true>(a, st);  // 17 x 17
     switch (variant) {
         case 1: return launch_t<7, 7, 128, 2, 12, 8, 2, false>(a, st);  // no L2 cache hints
         default: return launch_t<7, 7, 128, 2, 12, 8, 2, true>(a, st);

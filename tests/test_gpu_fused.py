@@ -223,3 +223,22 @@ def test_rowres_column_split_edges(w):
     res = rlDeconvolve(f, psf, RlConfig(iterations=12, op=K.Box1dSliding))
     ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, 12, O.BOX1D_SLIDING)
     assert W.max_rel(res.image, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("m", [9, 17])
+@pytest.mark.parametrize("w,h,it", [(1024, 768, 12), (37, 23, 5), (5, 3, 4), (513, 129, 7), (2050, 300, 2),
+                                    (600, 1, 3), (8192, 20, 3)])
+def test_fused_other_boxes_match_oracle(m, w, h, it):
+    """The one-launch iteration for the centred 9 x 9 and 17 x 17 boxes
+    (generic window sums, 9- / 17-row vertical rings)."""
+    from paper_1304_7211_b200 import RlSolver
+    from paper_1304_7211_b200.psf import makeBoxPsf
+    psf = makeBoxPsf(m, m)
+    rng = np.random.default_rng(w * 7 + h + m)
+    g = rng.uniform(0.05, 1.0, size=(h, w)).astype(np.float32)
+    f = np.maximum(W.blur_replicate(g, psf) + rng.normal(0, 0.01, size=g.shape), 1e-6).astype(np.float32)
+    assert RlSolver(psf, RlConfig(iterations=it, op=K.Box2dSliding), w, h).engine() == "fused"
+    res = rlDeconvolve(f, psf, RlConfig(iterations=it, op=K.Box2dSliding))
+    ref, mc, _ = O.rl_deconvolve(f.astype(np.float64), psf, it, O.BOX2D_SLIDING)
+    assert W.max_rel(res.image, ref) <= MAX_REL
+    np.testing.assert_allclose([r.maxAbsChange for r in res.trace.records], mc, rtol=1e-3, atol=1e-6)
