@@ -130,6 +130,8 @@ struct SelCache;
 void sel_destroy(SelCache* c);
 struct BatchCache;
 void batch_destroy(BatchCache* c);
+struct PipeCache;
+void pipe_destroy(PipeCache* c);
 }  // namespace
 
 struct fdg_ctx {
@@ -161,6 +163,9 @@ struct fdg_ctx {
     SelCache* sel = nullptr;
     // fdg_rl_deconvolve_batch: its chunked solver, planes and copy streams
     BatchCache* batch = nullptr;
+    // rlDeconvolve on page-locked host buffers, fused engine: copy streams,
+    // events and stamp slots of the time-skewed strip pipeline
+    PipeCache* pipe = nullptr;
     ~fdg_ctx();
 };
 
@@ -252,6 +257,7 @@ fdg_ctx::~fdg_ctx() {
     fdg_solver_destroy(rl_solver);
     sel_destroy(sel);
     batch_destroy(batch);
+    pipe_destroy(pipe);
     if (own_stream) cudaStreamDestroy(stream);
     a.release(), b.release(), c.release(), d.release(), m.release();
     tr_max.release(), tr_nan.release(), tr_inact.release(), first_bad.release(), tr_time.release();
@@ -812,6 +818,8 @@ struct EventPool {
     }
 };
 
+// 1: rlDeconvolve on large page-locked images runs the time-skewed strip pipeline
+std::atomic<int> g_pipeline{getenv("FDG_PIPELINE") ? atoi(getenv("FDG_PIPELINE")) : 1};
 }  // namespace
 
 int shard_set_loopback(int v);  // shard.cuh
@@ -832,6 +840,9 @@ int fdg_set_option(const char* name, int value) {
         const int prev = spans_jit_mode();
         set_spans_jit(value);
         return prev;
+    }
+    if (name && std::strcmp(name, "pipeline") == 0) {  // 1: time-skewed strip pipeline for large pinned images
+        return g_pipeline.exchange(value);
     }
     if (name && std::strcmp(name, "shard_loopback") == 0) return shard_set_loopback(value);
     if (name && std::strcmp(name, "shard_bands") == 0) return shard_set_bands(value);
@@ -1437,6 +1448,221 @@ int rl_step_impl(fdg_ctx* ctx, const fdg_plan* fwd, const fdg_plan* adj, const f
     }
     return FDG_OK;
 }
+
+// ------------------------------------------------- time-skewed strip pipeline
+// rlDeconvolve on page-locked host buffers with the fused engine: the image is
+// cut into row strips and strip s runs ALL its iterations before strip s + 1
+// starts, its row range sliding up by D = 2 RY rows (the iteration's
+// dependency radius) every iteration:
+//
+//   strip s, iteration k:  rows [a_s - D k, a_{s+1} - D k)   (clipped to the
+//                          image; the first strip starts at row 0, the last
+//                          one ends at row H - 1 and grows)
+//
+// Iteration k of strip s reads u^k on rows [a_s - D (k + 1), a_{s+1} - D (k - 1)):
+// the part below a_s - D (k - 1) was written by strip s - 1 (finished), the
+// rest by strip s itself one iteration earlier -- so no halo is recomputed, the
+// two ping-pong planes suffice (a strip's later writes to a plane end exactly
+// where its lower neighbour's reads of that plane begin), and the loop of
+// rl.hpp:153-177 is evaluated pixel for pixel.  What it buys: strip s needs
+// only rows < a_{s+1} + D of f, so the upload of the next strips overlaps the
+// iterations, and the rows of a finished strip are downloaded while the next
+// strips iterate.  A call pays for the first strip's upload, the iterations and
+// the last strip's download instead of upload + iterations + download.
+struct PipeCache {
+    cudaStream_t cin = nullptr, cout_ = nullptr;
+    std::vector<cudaEvent_t> ev;
+    DevBuf<unsigned long long> ts;  // [0] start, [1 + s K + k] end of (strip s, iteration k)
+    unsigned long long* h_ts = nullptr;
+    size_t h_cap = 0;
+    int device = 0;
+    ~PipeCache() {
+        DevScope ds;
+        ds.enter(device);
+        if (cin) cudaStreamSynchronize(cin), cudaStreamDestroy(cin);
+        if (cout_) cudaStreamSynchronize(cout_), cudaStreamDestroy(cout_);
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+        if (h_ts) cudaFreeHost(h_ts);
+        ts.release();
+    }
+};
+void pipe_destroy(PipeCache* c) { delete c; }
+
+
+// Strip boundaries a_0 = 0 < a_1 < ... < a_n = H at iteration 0.  Short first
+// strip (its upload is not hidden), growing strips (the upload runs ~5x faster
+// than the iterations, so it stays ahead), a short last strip (its download is
+// not hidden; it grows by D rows per iteration).  FDG_PIPE_STRIPS="h0,h1,..."
+// overrides the heights (the last strip takes the rest).
+std::vector<int> pipe_strips(int H, int D, int iters) {
+    std::vector<int> a{0};
+    if (const char* e = getenv("FDG_PIPE_STRIPS")) {
+        for (const char* p = e; *p;) {
+            const int h = atoi(p);
+            if (h > 0 && a.back() + h < H) a.push_back(a.back() + h);
+            while (*p && *p != ',') ++p;
+            if (*p == ',') ++p;
+        }
+        a.push_back(H);
+        return a;
+    }
+    // Measured on config 4 (16384^2, 100 iterations, scripts/pipe_tune.sh):
+    // every strip costs ~2.5 ms of extra halo rows and pipeline fills over its
+    // 100 launches, so few strips; the last one starts at 64 rows (it ends
+    // D (iters - 1) rows taller, and all of those download after the loop).
+    (void)iters;
+    const int last = std::min(64, std::max(4, H / 8));
+    const int body = H - last;
+    int h = std::max(std::min(512, std::max(H / 4, 4 * D)), std::min(1024, H / 16));
+    const int cap = std::max(h, H * 3 / 8);
+    while (a.back() + h < body) {
+        a.push_back(a.back() + h);
+        h = std::min(cap, 4 * h);
+    }
+    // fold a short remainder into the previous strip
+    if (a.size() > 2 && body - a.back() < (a.back() - a[a.size() - 2]) / 4) a.pop_back();
+    if (body > a.back()) a.push_back(body);
+    a.push_back(H);
+    return a;
+}
+
+// option "pipeline": 0 off, 1 large images only (>= 48 Mpx, >= 4096 rows: the
+// strips must be tall enough to keep every SM busy), 2 whenever the engine and
+// the buffers allow (tests)
+bool pipe_applies(const fdg_solver* sv, int W, int H, int iters, const float* f, const float* u_out) {
+    const int mode = g_pipeline.load();
+    if (mode < 1 || iters < 1 || sv->batch != 1) return false;
+    if (!use_fused(sv->fwd.get()) || !fused_halo_ok(W) || use_rowres(sv->fwd.get(), W)) return false;
+    if (mode == 1 && ((long long)W * H < (48ll << 20) || H < 4096)) return false;
+    return !pageable(f) && !pageable(u_out);
+}
+
+// The whole call: uploads, validation, iterations, downloads, trace.  mc / nf
+// / sec: per iteration (sec = the iteration's launches summed over strips).
+int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, float* df, float* du, int pitch,
+                 std::vector<float>* mc, std::vector<int>* nf, std::vector<double>* sec) {
+    const int W = sv->W, H = sv->H, K = sv->cfg.iterations;
+    const int D = 2 * (sv->fwd->dev.my / 2);
+    const std::vector<int> a = pipe_strips(H, D, K);
+    const int n = (int)a.size() - 1;
+    if (!ctx->pipe) {
+        auto pc = std::make_unique<PipeCache>();
+        pc->device = ctx->device;
+        CK(cudaStreamCreateWithFlags(&pc->cin, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&pc->cout_, cudaStreamNonBlocking));
+        ctx->pipe = pc.release();
+    }
+    PipeCache* pc = ctx->pipe;
+    while ((int)pc->ev.size() < 2 * n + 1) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        pc->ev.push_back(e);
+    }
+    const size_t nts = 1 + (size_t)n * K;
+    CK(pc->ts.ensure(nts));
+    if (pc->h_cap < nts) {
+        if (pc->h_ts) cudaFreeHost(pc->h_ts);
+        pc->h_ts = nullptr;
+        CK(cudaHostAlloc(&pc->h_ts, nts * sizeof(unsigned long long), cudaHostAllocDefault));
+        pc->h_cap = nts;
+    }
+    HaloPlanes hp;
+    hp.pitch = (W + fused_halo_left() + fused_halo_right() + 31) & ~31;
+    hp.stride = (long long)hp.pitch * H;
+    CK(sv->uh.ensure(2 * (size_t)hp.stride + 32));
+    hp.p[0] = sv->uh.p + fused_halo_left();
+    hp.p[1] = hp.p[0] + (size_t)hp.stride;
+
+    cudaStream_t comp = ctx->stream;
+    const size_t row = (size_t)W * 4;
+    // diagnostics (FDG_PIPE_DEBUG): timed events per strip on the three streams
+    static const bool dbg = getenv("FDG_PIPE_DEBUG") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    if (dbg) {
+        tev.resize(3 * n + 1);
+        for (cudaEvent_t& e : tev) CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(tev[3 * n], comp));
+    }
+    // uploads: strip s needs rows < a_{s+1} + D of f (u0 = f incl. its halo)
+    CK(cudaEventRecord(pc->ev[2 * n], comp));
+    CK(cudaStreamWaitEvent(pc->cin, pc->ev[2 * n], 0));
+    std::vector<int> c(n + 1, 0);
+    for (int s = 0; s < n; ++s) {
+        c[s + 1] = s == n - 1 ? H : std::min(H, a[s + 1] + D);
+        if (c[s + 1] > c[s])
+            CK(cudaMemcpy2DAsync(df + (size_t)c[s] * pitch, (size_t)pitch * 4, f + (size_t)c[s] * W, row, row,
+                                 c[s + 1] - c[s], cudaMemcpyHostToDevice, pc->cin));
+        CK(cudaEventRecord(pc->ev[2 * s], pc->cin));
+        if (dbg) CK(cudaEventRecord(tev[3 * s], pc->cin));
+    }
+    CK(ctx->first_bad.ensure(2));
+    if (!ctx->h_bad) CK(cudaHostAlloc(&ctx->h_bad, 2 * sizeof(unsigned long long), cudaHostAllocDefault));
+    if (int st = solver_reset_trace(sv)) return st;
+    CK(cudaMemsetAsync(pc->ts.p, 0, nts * sizeof(unsigned long long), comp));
+    const TraceSlots tr = solver_slots(sv);
+    for (int s = 0; s < n; ++s) {
+        CK(cudaStreamWaitEvent(comp, pc->ev[2 * s], 0));
+        if (s == 0) {
+            CK(launch_stamp(pc->ts.p, comp));
+            ctx->launches += 1;
+        }
+        // rl.hpp:78-83 on the rows that just arrived; the verdict is read at the end
+        CK(launch_validate_rows(df, W, c[s], c[s + 1] - c[s], pitch, ctx->first_bad.p, s == 0, comp));
+        ctx->launches += 1;
+        int lo = 0, hi = 0;
+        for (int k = 0; k < K; ++k) {
+            lo = s == 0 ? 0 : std::max(0, a[s] - D * k);
+            hi = s == n - 1 ? H : std::max(0, a[s + 1] - D * k);
+            if (hi <= lo) continue;
+            const bool last = k == K - 1;
+            const float* src = k == 0 ? df : hp.p[(k - 1) & 1];
+            float* dst = last ? du : hp.p[k & 1];
+            const int slot = std::min(k, sv->ntrace - 1);
+            int r = run_fused(ctx, sv->fwd.get(), src, df, dst, pitch, W, H, 1, (long long)pitch * H, &sv->cfg,
+                              tr.mc_at(slot), tr.nf_at(slot), pc->ts.p + 1 + (size_t)s * K + k, comp, lo, hi, 0, H - 1,
+                              &hp, k > 0, !last);
+            if (r) return r;
+        }
+        // the strip's final rows go home while the next strips iterate
+        CK(cudaEventRecord(pc->ev[2 * s + 1], comp));
+        if (dbg) CK(cudaEventRecord(tev[3 * s + 1], comp));
+        if (hi > lo) {
+            CK(cudaStreamWaitEvent(pc->cout_, pc->ev[2 * s + 1], 0));
+            CK(cudaMemcpy2DAsync(u_out + (size_t)lo * W, row, du + (size_t)lo * pitch, (size_t)pitch * 4, row, hi - lo,
+                                 cudaMemcpyDeviceToHost, pc->cout_));
+        }
+        if (dbg) CK(cudaEventRecord(tev[3 * s + 2], pc->cout_));
+    }
+    CK(cudaMemcpyAsync(ctx->h_bad, ctx->first_bad.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, comp));
+    CK(cudaMemcpyAsync(pc->h_ts, pc->ts.p, nts * sizeof(unsigned long long), cudaMemcpyDeviceToHost, comp));
+    // the caller's stream continues after the downloads
+    CK(cudaEventRecord(pc->ev[2 * n], pc->cout_));
+    CK(cudaStreamWaitEvent(comp, pc->ev[2 * n], 0));
+    sv->last_rowres = false;
+    std::vector<double> unused;
+    if (int st = solver_trace(sv, K, mc, nf, &unused)) return st;  // synchronises comp (hence cout_)
+    if (dbg) {
+        for (int s = 0; s < n; ++s) {
+            float t0 = 0, t1 = 0, t2 = 0;
+            cudaEventElapsedTime(&t0, tev[3 * n], tev[3 * s]);
+            cudaEventElapsedTime(&t1, tev[3 * n], tev[3 * s + 1]);
+            cudaEventElapsedTime(&t2, tev[3 * n], tev[3 * s + 2]);
+            fprintf(stderr, "[fdg pipe] strip %d rows [%d, %d): upload done %.2f ms, iterations done %.2f ms, download done %.2f ms\n",
+                    s, a[s], a[s + 1], t0, t1, t2);
+        }
+        for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
+    sec->assign(K, 0.0);
+    unsigned long long prev = pc->h_ts[0];
+    for (int s = 0; s < n; ++s)
+        for (int k = 0; k < K; ++k) {
+            const unsigned long long t = pc->h_ts[1 + (size_t)s * K + k];
+            if (!t) continue;  // empty range: no launch
+            if (prev && t > prev) (*sec)[k] += (double)(t - prev) * 1e-9;
+            prev = t;
+        }
+    return FDG_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -1493,6 +1719,21 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     CK(ctx->tr_inact.ensure(iters + 1));
     float *df = ctx->a.p, *du = ctx->b.p, *dq = ctx->c.p;
     pt.mark("alloc");
+    if (sv && pipe_applies(sv, W, H, iters, f, u_out)) {
+        std::vector<float> mc;
+        std::vector<int> nf;
+        std::vector<double> sec;
+        if ((st = rl_pipelined(ctx, sv, f, u_out, df, du, pitch, &mc, &nf, &sec))) return st;
+        pt.mark("pipelined");
+        const unsigned long long nf0 = ctx->h_bad[0], neg0 = ctx->h_bad[1];
+        if (nf0 != ~0ull && nf0 <= neg0) return set_err(FDG_EINVAL, "rlDeconvolve: input image has non-finite pixels");
+        if (neg0 != ~0ull) return set_err(FDG_EINVAL, "rlDeconvolve: input image must be nonnegative");
+        for (int k = 0; k < iters; ++k) {
+            if (nf[k]) return set_err(FDG_ENAN, "rlDeconvolve: NaN in iterate at iteration " + std::to_string(k + 1));
+            if (trace) trace[k] = {k + 1, 0.0, (double)mc[k], sec[k]};
+        }
+        return FDG_OK;
+    }
     if ((st = h2d(ctx->stg, df, pitch, f, W, H, s))) return st;
     if (!sv && (st = validate_device(ctx, df, W, H, pitch, "rlDeconvolve"))) return st;
     pt.mark("h2d+validate");

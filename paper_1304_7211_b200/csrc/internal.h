@@ -187,6 +187,8 @@ cudaError_t launch_pad_halo(const float* src, int pitch_src, long long bs_src, f
                             long long bs_dst, int W, int H, int batch, cudaStream_t st);
 // first non-finite / first negative row-major index (~0 if none) -> out[0..1]
 cudaError_t launch_validate(const float* f, int W, int H, int pitch, unsigned long long* out, cudaStream_t st);
+cudaError_t launch_validate_rows(const float* f, int W, int r0, int rows, int pitch, unsigned long long* out, int init,
+                                 cudaStream_t st);
 // one thread writes %globaltimer to *t (start stamp of a timed RL loop)
 cudaError_t launch_stamp(unsigned long long* t, cudaStream_t st);
 cudaError_t launch_count_inactive(const uint8_t* active, size_t n, unsigned long long* out,

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     const long long pitch = a.pitch, pitch_u = a.pitch_u, pitch_o = a.pitch_o;
     // one column strip x0, output rows [yb0, yb1): fresh barriers, every role
     // runs its pipeline to the end of the segment
-    auto run_segment = [&](const int x0, const int yb0, const int yb1) {
+    auto run_segment = [&](const int x0, const int xown, const int yb0, const int yb1) {
         const int qr_lo = max(a.ylo, yb0 - RY), qr_hi = min(a.yhi, yb1 - 1 + RY);
         const int nq = qr_hi - qr_lo + 1;  // q rows this band needs
         const int j0 = qr_lo - RY;         // first streamed u row (may be < 0: clamped)
@@ -498,7 +498,11 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         const int tb = tid - NT;
         const int lane = tid & 31;
         const int oc = x0 + 4 * tb;
-        const bool has_out = tb < G::NB && oc < a.W;  // lanes past the strip compute, never store
+        // lanes past the strip compute, never store; neither do the lanes of a
+        // shifted last strip left of the columns it owns (xown): the neighbour's
+        // CTA computes those from another segment start (its running sums round
+        // differently), and two writers would make the result depend on timing
+        const bool has_out = tb < G::NB && oc < a.W && oc >= xown;
         const bool full_store = oc + 3 < a.W;
         // replicated halo columns of u_out: the owners of columns 0 / W-1
         // replicated halo columns of u_out (halo mode needs W % 4 == 0): B warp 0
@@ -670,11 +674,11 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         const int r1 = (int)min((long long)rows, r0 + (end - p));
         if (!first) reset_barriers();
         // the last strip is shifted left to end at the image edge (overlapping
-        // its neighbour, whose columns it rewrites with identical values): a
+        // its neighbour, whose columns it computes but does not store): a
         // strip reaching far past column W-1 makes the producer replicate
         // hundreds of columns per row and straggles the whole launch
         const int xs = a.W > G::CW ? min(sx * G::CW, (a.W - G::CW + 3) & ~3) : 0;
-        run_segment(xs, ybase + r0, ybase + r1);
+        run_segment(xs, a.W > G::CW ? sx * G::CW : 0, ybase + r0, ybase + r1);
         p += r1 - r0;
     }
 #ifdef FDG_FUSED_PROBE

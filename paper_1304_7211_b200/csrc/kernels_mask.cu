@@ -181,7 +181,8 @@ namespace fdg {
 namespace {
 // first non-finite / first negative row-major index: float4 per thread
 // (rows are 16-byte aligned, pitch % 4 == 0), one integer division per 4 px
-__global__ void k_validate(const float* f, int W, int H, int pitch, unsigned long long* out) {
+__global__ void k_validate(const float* f, int W, int H, int pitch, unsigned long long* out,
+                           unsigned long long first = 0) {
     unsigned long long bad_nf = ~0ull, bad_neg = ~0ull;
     const long long nq = (W + 3) / 4;
     const long long n = nq * H;
@@ -200,7 +201,7 @@ __global__ void k_validate(const float* f, int W, int H, int pitch, unsigned lon
 #pragma unroll
             for (int e = 0; e < 4; ++e) v[e] = x + e < W ? row[x + e] : 0.f;
         }
-        const unsigned long long base = (unsigned long long)y * W + x;
+        const unsigned long long base = first + (unsigned long long)y * W + x;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             if (!isfinite(v[e])) bad_nf = min(bad_nf, base + e);
@@ -228,6 +229,16 @@ __global__ void k_fill_u64(unsigned long long* p, int n) {
 cudaError_t launch_validate(const float* f, int W, int H, int pitch, unsigned long long* out, cudaStream_t st) {
     k_fill_u64<<<1, 32, 0, st>>>(out, 2);
     k_validate<<<1184, 256, 0, st>>>(f, W, H, pitch, out);
+    return cudaGetLastError();
+}
+
+// rows [r0, r0 + rows) of an image whose row 0 is f (indices stay those of
+// the whole image); init: reset the two slots first
+cudaError_t launch_validate_rows(const float* f, int W, int r0, int rows, int pitch, unsigned long long* out, int init,
+                                 cudaStream_t st) {
+    if (init) k_fill_u64<<<1, 32, 0, st>>>(out, 2);
+    if (rows > 0)
+        k_validate<<<592, 256, 0, st>>>(f + (size_t)r0 * pitch, W, rows, pitch, out, (unsigned long long)r0 * W);
     return cudaGetLastError();
 }
 }  // namespace fdg

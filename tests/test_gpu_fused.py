@@ -242,3 +242,14 @@ def test_fused_other_boxes_match_oracle(m, w, h, it):
     ref, mc, _ = O.rl_deconvolve(f.astype(np.float64), psf, it, O.BOX2D_SLIDING)
     assert W.max_rel(res.image, ref) <= MAX_REL
     np.testing.assert_allclose([r.maxAbsChange for r in res.trace.records], mc, rtol=1e-3, atol=1e-6)
+
+
+def test_fused_repeat_calls_are_bit_identical():
+    """Work-balanced segments with the last column strip shifted to end at the
+    image edge (2000 = 4 x 496 + 16): the overlapped columns have one writer,
+    so the result does not depend on which CTA finishes last."""
+    f, psf = _input(2000, 8000, 77)
+    cfg = RlConfig(iterations=6, op=K.Box2dSliding)
+    a = rlDeconvolve(f, psf, cfg).image
+    for _ in range(3):
+        assert np.array_equal(a, rlDeconvolve(f, psf, cfg).image)
