@@ -402,6 +402,9 @@ def run_ours(args, cfg, world, rank, local):
         e2e = {"value": W_ * H_ * iters / e2e_s / 1e6, "unit": "Mpx*it/s", "h2d_bytes_per_step": int(f_host.nbytes),
                "d2h_bytes_per_step": int(res.image.nbytes),
                "api": "paper_1304_7211_b200.rlDeconvolve (C ABI fdg_rl_deconvolve, page-locked host buffers in and out)"}
+        ns = ctx.last_schedule()
+        e2e["schedule"] = (f"time-skewed pipeline over {ns} row strips (uploads / downloads overlap the iterations)"
+                           if ns else "upload, iterate, download")
     elif shard is not None:
         # this rank's strip through the sharded entry point with host buffers
         # (H2D of its f rows, D2H of its u rows every step); max over ranks

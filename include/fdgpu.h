@@ -100,6 +100,10 @@ int fdg_get_device(int* device);
  *   "spans": GenericBox span-table kernels (kernels_spans.cu): 0 = by size
  *            (tile kernel up to 4.5 Mpx per launch, default), 1 = tile
  *            kernel, 2 = marching kernel.
+ *   "pipeline": fdg_rl_deconvolve on page-locked host buffers with the fused
+ *            engine runs as time-skewed row strips whose uploads / downloads
+ *            overlap the iterations: 1 = images >= 48 Mpx and >= 4096 rows
+ *            (default), 0 = never, 2 = whenever engine and buffers allow.
  * Returns the previous value, or -1 for an unknown name. */
 int fdg_set_option(const char* name, int value);
 
@@ -117,6 +121,9 @@ int fdg_ctx_set_stream(fdg_ctx* ctx, void* cuda_stream);
 int fdg_ctx_synchronize(fdg_ctx* ctx);
 /* number of kernel launches issued through this context so far */
 uint64_t fdg_ctx_launch_count(const fdg_ctx* ctx);
+/* schedule of the context's last fdg_rl_deconvolve: 0 = upload, iterate,
+ * download; n >= 2 = time-skewed pipeline over n row strips */
+int fdg_ctx_last_schedule(const fdg_ctx* ctx);
 
 /* ---- plan logic (host only; no device needed) ----------------------- */
 /* dispatch(), convolve.hpp:627-643 -> *kind, or FDG_EINVAL naming op+PSF */

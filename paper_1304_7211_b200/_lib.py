@@ -105,6 +105,7 @@ def lib():
             "fdg_ctx_set_stream": (C.c_int, [vp, vp]),
             "fdg_ctx_synchronize": (C.c_int, [vp]),
             "fdg_ctx_launch_count": (C.c_uint64, [vp]),
+            "fdg_ctx_last_schedule": (C.c_int, [vp]),
             "fdg_dispatch": (C.c_int, [D, C.c_int, ip]),
             "fdg_operator_accepts": (C.c_int, [C.c_int, D, ip]),
             "fdg_plan_create": (C.c_int, [vp, D, C.c_int, C.POINTER(vp)]),
@@ -255,6 +256,11 @@ class Context:
 
     def launch_count(self) -> int:
         return int(lib().fdg_ctx_launch_count(self.h))
+
+    def last_schedule(self) -> int:
+        """0: the last rlDeconvolve uploaded, iterated, downloaded; n >= 2: it
+        ran as a time-skewed pipeline over n row strips."""
+        return int(lib().fdg_ctx_last_schedule(self.h))
 
     def __del__(self):
         try:

@@ -139,6 +139,7 @@ struct fdg_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     uint64_t launches = 0;
+    int last_schedule = 0;  // last fdg_rl_deconvolve: 0 plain, n = pipelined over n strips
     // one caller at a time per context (scratch, staging, stream, cached
     // solver); recursive: entry points call each other
     std::recursive_mutex mu;
@@ -920,6 +921,7 @@ int fdg_ctx_synchronize(fdg_ctx* ctx) {
 }
 
 uint64_t fdg_ctx_launch_count(const fdg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int fdg_ctx_last_schedule(const fdg_ctx* ctx) { return ctx ? ctx->last_schedule : 0; }
 
 int fdg_dispatch(const fdg_psf_desc* desc, int preference, int* kind) {
     HostPsf h;
@@ -1545,6 +1547,7 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, flo
     const int D = 2 * (sv->fwd->dev.my / 2);
     const std::vector<int> a = pipe_strips(H, D, K);
     const int n = (int)a.size() - 1;
+    ctx->last_schedule = n;
     if (!ctx->pipe) {
         auto pc = std::make_unique<PipeCache>();
         pc->device = ctx->device;
@@ -1719,6 +1722,7 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     CK(ctx->tr_inact.ensure(iters + 1));
     float *df = ctx->a.p, *du = ctx->b.p, *dq = ctx->c.p;
     pt.mark("alloc");
+    ctx->last_schedule = 0;
     if (sv && pipe_applies(sv, W, H, iters, f, u_out)) {
         std::vector<float> mc;
         std::vector<int> nf;

@@ -2,8 +2,8 @@
 //
 // k_tile_compact: one CTA per 64x64 dense tile; each thread owns a 4x4 pixel
 //   block, flags it when any pixel is active, and the CTA compacts the
-//   flagged block ids in ascending (row-major) order with warp ballots +
-//   popc prefix sums.  The thinned dense kernel consumes these per-tile lists
+//   flagged block ids (warp ballots + popc prefix sums) in a bank-friendly
+//   round-robin order over the block columns.  The thinned dense kernel consumes these per-tile lists
 //   (tiles with no active block exit immediately).  The same pass counts the
 //   inactive pixels of the iteration for RlTrace.inactiveFraction.
 // k_row_count / k_row_emit: the reference's row-major run walk
@@ -19,7 +19,7 @@ constexpr int TD = 64;
 __global__ void __launch_bounds__(256) k_tile_compact(const uint8_t* act, int W, int H, int pitch,
                                                       int* tile_blocks, int* tile_count,
                                                       unsigned long long* inactive) {
-    __shared__ int warp_n[8];
+    __shared__ int warp_bn[8][8];  // per warp: active blocks per bucket
     __shared__ unsigned long long warp_inact[8];
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int tile = blockIdx.y * gridDim.x + blockIdx.x;
@@ -39,21 +39,35 @@ __global__ void __launch_bounds__(256) k_tile_compact(const uint8_t* act, int W,
     }
     const unsigned ball = __ballot_sync(0xffffffffu, any);
     const int cnt_inact = __reduce_add_sync(0xffffffffu, nin);
-    if (lane == 0) {
-        warp_n[wid] = __popc(ball);
-        warp_inact[wid] = (unsigned long long)cnt_inact;
-    }
+    // List order: the dense kernel gives list entry i to thread i, and its
+    // float4 tile loads are bank-conflict free only when the 8 lanes of a
+    // quarter warp read 8 different 16-byte columns -- block column bx mod 8
+    // (tile rows are a multiple of 32 floats apart).  A plain ascending list
+    // puts arbitrary bx side by side (measured: the masked pass then runs
+    // shared-memory bound and skipping blocks buys nothing), so the blocks are
+    // dealt round-robin from 8 buckets j = bx mod 8: entry (r, j) = the r-th
+    // active block of bucket j, entries in (r, j) order with the absent ones
+    // squeezed out.  Any 8 consecutive entries then hold 8 different buckets
+    // except where a bucket ran out.
+    const int j = t & 7;  // = bx & 7
+    const unsigned bmask = 0x01010101u << j;
+    if (lane < 8) warp_bn[wid][lane] = __popc(ball & (0x01010101u << lane));
+    if (lane == 0) warp_inact[wid] = (unsigned long long)cnt_inact;
     __syncthreads();
-    int base = 0;
-    for (int w = 0; w < wid; ++w) base += warp_n[w];
-    if (any) tile_blocks[(long long)tile * 256 + base + __popc(ball & ((1u << lane) - 1u))] = t;
+    int r = __popc(ball & bmask & ((1u << lane) - 1u));  // rank inside the bucket
+    for (int w = 0; w < wid; ++w) r += warp_bn[w][j];
+    int total = 0, before = 0;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+        int n = 0;
+        for (int w = 0; w < 8; ++w) n += warp_bn[w][jj];
+        total += n;
+        before += min(n, r) + (jj < j && n > r);
+    }
+    if (any) tile_blocks[(long long)tile * 256 + before] = t;
     if (t == 0) {
-        int total = 0;
         unsigned long long ni = 0;
-        for (int w = 0; w < 8; ++w) {
-            total += warp_n[w];
-            ni += warp_inact[w];
-        }
+        for (int w = 0; w < 8; ++w) ni += warp_inact[w];
         tile_count[tile] = total;
         if (inactive && ni) atomicAdd(inactive, ni);
     }

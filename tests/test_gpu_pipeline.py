@@ -111,8 +111,10 @@ def test_pipelined_is_the_path_taken_and_matches_plain():
     rlDeconvolve(fp, psf, cfg, ctx=ctx, out=o2)
     assert np.array_equal(o1, o2)
     assert n1 - n0 >= 3 * 10  # 3 strips x 10 iterations (+ stamp, validation)
+    assert ctx.last_schedule() == 3
     _lib.lib().fdg_set_option(b"pipeline", 0)
     rlDeconvolve(fp, psf, cfg, ctx=ctx, out=o3)
+    assert ctx.last_schedule() == 0
     assert W.max_rel(o1, o3.astype(np.float64)) <= 2e-5
 
 
