@@ -100,8 +100,8 @@ int fdg_get_device(int* device);
  *   "spans": GenericBox span-table kernels (kernels_spans.cu): 0 = by size
  *            (tile kernel up to 4.5 Mpx per launch, default), 1 = tile
  *            kernel, 2 = marching kernel.
- *   "pipeline": fdg_rl_deconvolve on page-locked host buffers with the fused
- *            engine runs as time-skewed row strips whose uploads / downloads
+ *   "pipeline": fdg_rl_deconvolve with the fused engine runs as time-skewed
+ *            row strips whose uploads / downloads (pageable buffers: staged)
  *            overlap the iterations: 1 = images >= 48 Mpx and >= 4096 rows
  *            (default), 0 = never, 2 = whenever engine and buffers allow.
  * Returns the previous value, or -1 for an unknown name. */

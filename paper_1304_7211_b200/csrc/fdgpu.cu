@@ -1452,8 +1452,8 @@ int rl_step_impl(fdg_ctx* ctx, const fdg_plan* fwd, const fdg_plan* adj, const f
 }
 
 // ------------------------------------------------- time-skewed strip pipeline
-// rlDeconvolve on page-locked host buffers with the fused engine: the image is
-// cut into row strips and strip s runs ALL its iterations before strip s + 1
+// rlDeconvolve on host buffers with the fused engine: the image is cut into
+// row strips and strip s runs ALL its iterations before strip s + 1
 // starts, its row range sliding up by D = 2 RY rows (the iteration's
 // dependency radius) every iteration:
 //
@@ -1536,7 +1536,11 @@ bool pipe_applies(const fdg_solver* sv, int W, int H, int iters, const float* f,
     if (mode < 1 || iters < 1 || sv->batch != 1) return false;
     if (!use_fused(sv->fwd.get()) || !fused_halo_ok(W) || use_rowres(sv->fwd.get(), W)) return false;
     if (mode == 1 && ((long long)W * H < (48ll << 20) || H < 4096)) return false;
-    return !pageable(f) && !pageable(u_out);
+    // in-place calls (the result over the input): downloads would land in
+    // rows whose upload may still be queued
+    const char *fa = reinterpret_cast<const char*>(f), *ua = reinterpret_cast<const char*>(u_out);
+    const size_t bytes = (size_t)W * H * sizeof(float);
+    return !(fa < ua + bytes && ua < fa + bytes);
 }
 
 // The whole call: uploads, validation, iterations, downloads, trace.  mc / nf
@@ -1586,18 +1590,37 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, flo
         for (cudaEvent_t& e : tev) CK(cudaEventCreate(&e));
         CK(cudaEventRecord(tev[3 * n], comp));
     }
-    // uploads: strip s needs rows < a_{s+1} + D of f (u0 = f incl. its halo)
+    // uploads: strip s needs rows < a_{s+1} + D of f (u0 = f incl. its halo).
+    // Page-locked input: every upload is queued up front.  Pageable input goes
+    // through the context's pinned staging chunks (h2d: a multi-threaded host
+    // copy per chunk, which occupies this thread), so strip s + 1 is staged
+    // right after strip s's launches are queued, while the device works on them;
+    // likewise a pageable result is fetched (d2h, blocking) one strip late.
+    const bool pin_in = !pageable(f), pin_out = !pageable(u_out);
     CK(cudaEventRecord(pc->ev[2 * n], comp));
     CK(cudaStreamWaitEvent(pc->cin, pc->ev[2 * n], 0));
-    std::vector<int> c(n + 1, 0);
-    for (int s = 0; s < n; ++s) {
-        c[s + 1] = s == n - 1 ? H : std::min(H, a[s + 1] + D);
+    std::vector<int> c(n + 1, 0), flo(n, 0), fhi(n, 0);
+    for (int s = 0; s < n; ++s) c[s + 1] = s == n - 1 ? H : std::min(H, a[s + 1] + D);
+    auto upload = [&](int s) -> int {
         if (c[s + 1] > c[s])
-            CK(cudaMemcpy2DAsync(df + (size_t)c[s] * pitch, (size_t)pitch * 4, f + (size_t)c[s] * W, row, row,
-                                 c[s + 1] - c[s], cudaMemcpyHostToDevice, pc->cin));
+            if (int st = h2d(ctx->stg, df + (size_t)c[s] * pitch, pitch, f + (size_t)c[s] * W, W, c[s + 1] - c[s], pc->cin))
+                return st;
         CK(cudaEventRecord(pc->ev[2 * s], pc->cin));
         if (dbg) CK(cudaEventRecord(tev[3 * s], pc->cin));
-    }
+        return FDG_OK;
+    };
+    auto download = [&](int s) -> int {  // the strip's final rows, after its last launch
+        if (fhi[s] > flo[s]) {
+            CK(cudaStreamWaitEvent(pc->cout_, pc->ev[2 * s + 1], 0));
+            if (int st = d2h(ctx->stg, u_out + (size_t)flo[s] * W, du + (size_t)flo[s] * pitch, pitch, W,
+                             fhi[s] - flo[s], pc->cout_))
+                return st;
+        }
+        if (dbg) CK(cudaEventRecord(tev[3 * s + 2], pc->cout_));
+        return FDG_OK;
+    };
+    for (int s = 0; s < (pin_in ? n : 1); ++s)
+        if (int st = upload(s)) return st;
     CK(ctx->first_bad.ensure(2));
     if (!ctx->h_bad) CK(cudaHostAlloc(&ctx->h_bad, 2 * sizeof(unsigned long long), cudaHostAllocDefault));
     if (int st = solver_reset_trace(sv)) return st;
@@ -1612,10 +1635,11 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, flo
         // rl.hpp:78-83 on the rows that just arrived; the verdict is read at the end
         CK(launch_validate_rows(df, W, c[s], c[s + 1] - c[s], pitch, ctx->first_bad.p, s == 0, comp));
         ctx->launches += 1;
-        int lo = 0, hi = 0;
         for (int k = 0; k < K; ++k) {
-            lo = s == 0 ? 0 : std::max(0, a[s] - D * k);
-            hi = s == n - 1 ? H : std::max(0, a[s + 1] - D * k);
+            const int lo = s == 0 ? 0 : std::max(0, a[s] - D * k);
+            const int hi = s == n - 1 ? H : std::max(0, a[s + 1] - D * k);
+            flo[s] = lo;
+            fhi[s] = hi;
             if (hi <= lo) continue;
             const bool last = k == K - 1;
             const float* src = k == 0 ? df : hp.p[(k - 1) & 1];
@@ -1626,16 +1650,21 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, flo
                               &hp, k > 0, !last);
             if (r) return r;
         }
-        // the strip's final rows go home while the next strips iterate
         CK(cudaEventRecord(pc->ev[2 * s + 1], comp));
         if (dbg) CK(cudaEventRecord(tev[3 * s + 1], comp));
-        if (hi > lo) {
-            CK(cudaStreamWaitEvent(pc->cout_, pc->ev[2 * s + 1], 0));
-            CK(cudaMemcpy2DAsync(u_out + (size_t)lo * W, row, du + (size_t)lo * pitch, (size_t)pitch * 4, row, hi - lo,
-                                 cudaMemcpyDeviceToHost, pc->cout_));
+        // the device is busy with strip s: stage the next upload, fault in the
+        // result pages, bring finished rows home
+        if (!pin_in && s + 1 < n)
+            if (int st = upload(s + 1)) return st;
+        if (s == std::min(1, n - 1)) prefault(u_out, (size_t)W * H * sizeof(float));
+        if (pin_out) {
+            if (int st = download(s)) return st;
+        } else if (s >= 1) {
+            if (int st = download(s - 1)) return st;
         }
-        if (dbg) CK(cudaEventRecord(tev[3 * s + 2], pc->cout_));
     }
+    if (!pin_out)
+        if (int st = download(n - 1)) return st;
     CK(cudaMemcpyAsync(ctx->h_bad, ctx->first_bad.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, comp));
     CK(cudaMemcpyAsync(pc->h_ts, pc->ts.p, nts * sizeof(unsigned long long), cudaMemcpyDeviceToHost, comp));
     // the caller's stream continues after the downloads

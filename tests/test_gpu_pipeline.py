@@ -118,11 +118,25 @@ def test_pipelined_is_the_path_taken_and_matches_plain():
     assert W.max_rel(o1, o3.astype(np.float64)) <= 2e-5
 
 
-def test_pipelined_pageable_buffers_take_the_plain_path():
-    f, psf = _input(512, 400, 11)
-    res = rlDeconvolve(f, psf, RlConfig(iterations=5, op=K.Box2dSliding))
-    ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, 5, O.BOX2D_SLIDING)
-    assert W.max_rel(res.image, ref) <= MAX_REL
+@pytest.mark.parametrize("w,h,it,strips,pin_in,pin_out", [
+    (512, 400, 5, "100,150", False, False),     # small pageable arrays: plain copies inside the pipeline
+    (2048, 9000, 3, "4500", False, False),      # > 32 MiB per strip: two staging chunks up and down
+    (2048, 9000, 3, "3000,3000", True, False),  # page-locked in, pageable out
+    (2048, 9000, 3, "3000,3000", False, True),
+])
+def test_pipelined_pageable_buffers(w, h, it, strips, pin_in, pin_out):
+    """Pageable buffers go through the context's pinned staging chunks, strip
+    by strip, behind the launches of the previous strip."""
+    from paper_1304_7211_b200._lib import Context
+    f, psf = _input(w, h, 11 + w + h)
+    os.environ["FDG_PIPE_STRIPS"] = strips
+    ctx = Context(0)
+    fin = _pinned(f) if pin_in else f
+    out = _pinned(np.zeros_like(f)) if pin_out else np.zeros_like(f)
+    rlDeconvolve(fin, psf, RlConfig(iterations=it, op=K.Box2dSliding), ctx=ctx, out=out)
+    assert ctx.last_schedule() == len(strips.split(",")) + 1
+    ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, it, O.BOX2D_SLIDING)
+    assert W.max_rel(out, ref) <= MAX_REL
 
 
 @pytest.mark.parametrize("bad,msg", [(-1.0, "nonnegative"), (np.nan, "non-finite"), (np.inf, "non-finite")])
@@ -144,3 +158,14 @@ def test_pipelined_first_offender_decides_the_message():
     f[10, 3] = np.nan
     with pytest.raises(_lib.FdgInvalidArgument, match="non-finite"):
         _run(f, psf, 3, "100,200")
+
+
+def test_pipelined_in_place_call_takes_the_plain_path():
+    from paper_1304_7211_b200._lib import Context
+    f, psf = _input(512, 400, 21)
+    ctx = Context(0)
+    buf = _pinned(f)
+    rlDeconvolve(buf, psf, RlConfig(iterations=5, op=K.Box2dSliding), ctx=ctx, out=buf)
+    assert ctx.last_schedule() == 0
+    ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, 5, O.BOX2D_SLIDING)
+    assert W.max_rel(buf, ref) <= MAX_REL
