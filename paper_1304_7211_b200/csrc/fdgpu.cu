@@ -1491,13 +1491,23 @@ struct PipeCache {
 void pipe_destroy(PipeCache* c) { delete c; }
 
 
-// Strip boundaries a_0 = 0 < a_1 < ... < a_n = H at iteration 0.  Short first
-// strip (its upload is not hidden), growing strips (the upload runs ~5x faster
-// than the iterations, so it stays ahead), a short last strip (its download is
-// not hidden; it grows by D rows per iteration).  FDG_PIPE_STRIPS="h0,h1,..."
-// overrides the heights (the last strip takes the rest).
+// Strip boundaries a_0 = 0 < a_1 < ... < a_{n-1} at iteration 0 (strip n - 1
+// always ends at row H - 1).  Short first strip (its upload is not hidden),
+// growing strips (the upload runs ~5x faster than the iterations, so it stays
+// ahead).  The last boundary may lie BELOW the image, a_{n-1} = H + D (k0 - 1):
+// clipped to H it makes the last strip empty until iteration k0, after which
+// it grows by D rows per iteration to D (K - k0) rows -- those are the rows
+// whose download nothing hides.  Measured on config 4
+// (profiles/r02_pipeline_strip_tuning.txt): a late tail saves 2 ms of short
+// launches but leaves the previous strip's 6 ms download with nothing to hide
+// behind, so the default is k0 = 0: a 64-row last strip from the start.
+// FDG_PIPE_STRIPS="h0,h1,..." overrides the heights (the last strip takes the
+// rest), FDG_PIPE_K0 the birth iteration.
 std::vector<int> pipe_strips(int H, int D, int iters) {
     std::vector<int> a{0};
+    const char* ek = getenv("FDG_PIPE_K0");
+    const int k0 = ek ? atoi(ek) : 0;
+    const bool late = k0 >= 1 && k0 < iters;
     if (const char* e = getenv("FDG_PIPE_STRIPS")) {
         for (const char* p = e; *p;) {
             const int h = atoi(p);
@@ -1505,15 +1515,13 @@ std::vector<int> pipe_strips(int H, int D, int iters) {
             while (*p && *p != ',') ++p;
             if (*p == ',') ++p;
         }
-        a.push_back(H);
+        if (ek && late) a.push_back(H + D * (k0 - 1));
         return a;
     }
     // Measured on config 4 (16384^2, 100 iterations, scripts/pipe_tune.sh):
-    // every strip costs ~2.5 ms of extra halo rows and pipeline fills over its
-    // 100 launches, so few strips; the last one starts at 64 rows (it ends
-    // D (iters - 1) rows taller, and all of those download after the loop).
-    (void)iters;
-    const int last = std::min(64, std::max(4, H / 8));
+    // every strip costs ~2 ms of extra halo rows and pipeline fills over its
+    // 100 launches, so few strips.
+    const int last = late ? 0 : std::min(64, std::max(4, H / 8));
     const int body = H - last;
     int h = std::max(std::min(512, std::max(H / 4, 4 * D)), std::min(1024, H / 16));
     const int cap = std::max(h, H * 3 / 8);
@@ -1523,8 +1531,10 @@ std::vector<int> pipe_strips(int H, int D, int iters) {
     }
     // fold a short remainder into the previous strip
     if (a.size() > 2 && body - a.back() < (a.back() - a[a.size() - 2]) / 4) a.pop_back();
-    if (body > a.back()) a.push_back(body);
-    a.push_back(H);
+    if (late)
+        a.push_back(H + D * (k0 - 1));
+    else if (body > a.back())
+        a.push_back(body);
     return a;
 }
 
@@ -1550,7 +1560,7 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, flo
     const int W = sv->W, H = sv->H, K = sv->cfg.iterations;
     const int D = 2 * (sv->fwd->dev.my / 2);
     const std::vector<int> a = pipe_strips(H, D, K);
-    const int n = (int)a.size() - 1;
+    const int n = (int)a.size();  // strip s = [a_s, a_{s+1}) at iteration 0, the last one to the image's end
     ctx->last_schedule = n;
     if (!ctx->pipe) {
         auto pc = std::make_unique<PipeCache>();
@@ -1600,7 +1610,7 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, flo
     CK(cudaEventRecord(pc->ev[2 * n], comp));
     CK(cudaStreamWaitEvent(pc->cin, pc->ev[2 * n], 0));
     std::vector<int> c(n + 1, 0), flo(n, 0), fhi(n, 0);
-    for (int s = 0; s < n; ++s) c[s + 1] = s == n - 1 ? H : std::min(H, a[s + 1] + D);
+    for (int s = 0; s < n; ++s) c[s + 1] = s == n - 1 ? H : std::max(c[s], std::min(H, a[s + 1] + D));
     auto upload = [&](int s) -> int {
         if (c[s + 1] > c[s])
             if (int st = h2d(ctx->stg, df + (size_t)c[s] * pitch, pitch, f + (size_t)c[s] * W, W, c[s + 1] - c[s], pc->cin))
@@ -1636,8 +1646,8 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, flo
         CK(launch_validate_rows(df, W, c[s], c[s + 1] - c[s], pitch, ctx->first_bad.p, s == 0, comp));
         ctx->launches += 1;
         for (int k = 0; k < K; ++k) {
-            const int lo = s == 0 ? 0 : std::max(0, a[s] - D * k);
-            const int hi = s == n - 1 ? H : std::max(0, a[s + 1] - D * k);
+            const int lo = s == 0 ? 0 : std::min(H, std::max(0, a[s] - D * k));
+            const int hi = s == n - 1 ? H : std::min(H, std::max(0, a[s + 1] - D * k));
             flo[s] = lo;
             fhi[s] = hi;
             if (hi <= lo) continue;
@@ -1679,8 +1689,8 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, flo
             cudaEventElapsedTime(&t0, tev[3 * n], tev[3 * s]);
             cudaEventElapsedTime(&t1, tev[3 * n], tev[3 * s + 1]);
             cudaEventElapsedTime(&t2, tev[3 * n], tev[3 * s + 2]);
-            fprintf(stderr, "[fdg pipe] strip %d rows [%d, %d): upload done %.2f ms, iterations done %.2f ms, download done %.2f ms\n",
-                    s, a[s], a[s + 1], t0, t1, t2);
+            fprintf(stderr, "[fdg pipe] strip %d from row %d: upload done %.2f ms, iterations done %.2f ms, download done %.2f ms\n",
+                    s, a[s], t0, t1, t2);
         }
         for (cudaEvent_t e : tev) cudaEventDestroy(e);
     }

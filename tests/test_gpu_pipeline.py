@@ -169,3 +169,16 @@ def test_pipelined_in_place_call_takes_the_plain_path():
     assert ctx.last_schedule() == 0
     ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, 5, O.BOX2D_SLIDING)
     assert W.max_rel(buf, ref) <= MAX_REL
+
+
+def test_pipelined_late_born_last_strip():
+    """FDG_PIPE_K0: the last boundary starts below the image, the last strip is
+    empty until iteration k0 and grows afterwards."""
+    f, psf = _input(512, 700, 31)
+    os.environ["FDG_PIPE_K0"] = "6"
+    try:
+        out, _ = _run(f, psf, 14, "200,250")
+    finally:
+        os.environ.pop("FDG_PIPE_K0", None)
+    ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, 14, O.BOX2D_SLIDING)
+    assert W.max_rel(out, ref) <= MAX_REL
