@@ -182,3 +182,12 @@ def test_pipelined_late_born_last_strip():
         os.environ.pop("FDG_PIPE_K0", None)
     ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, 14, O.BOX2D_SLIDING)
     assert W.max_rel(out, ref) <= MAX_REL
+
+
+def test_pipelined_nan_in_iterate_reported():
+    """rl.hpp:96-99,173 through the strip schedule: the NaN flag of an
+    iteration accumulates over the strips' launches."""
+    f = np.ones((700, 512), np.float32)
+    f[450:520, 100:300] = 3.0e38  # overflows the fp32 window sums in a late strip
+    with pytest.raises(_lib.FdgNaNError, match=r"rlDeconvolve: NaN in iterate at iteration \d+"):
+        _run(f, W.make_psf(W.CONFIGS["cfg4"].psf), 8, "100,200")
