@@ -86,10 +86,14 @@ inline RlTrace toTrace(const std::vector<fdg_rl_record>& recs) {
 inline fdg_ctx* contextOrNull() { return fdg_device_available() ? context() : nullptr; }
 
 /// rl.hpp:71-84 in the reference's order (config, then pixels in double)
-inline void validateRlInputs(const Image& f, const RlConfig& cfg, const char* where) {
+inline void validateRlConfig(const Image& f, const RlConfig& cfg, const char* where) {
     if (f.empty()) throw std::invalid_argument(std::string(where) + ": empty input image");
     if (cfg.iterations < 0) throw std::invalid_argument(std::string(where) + ": iterations must be >= 0");
     if (!(cfg.epsilonDiv > 0.0)) throw std::invalid_argument(std::string(where) + ": epsilonDiv must be positive");
+}
+
+inline void validateRlInputs(const Image& f, const RlConfig& cfg, const char* where) {
+    validateRlConfig(f, cfg, where);
     validatePixels(f, where);
 }
 
@@ -110,14 +114,16 @@ inline Image rlStep(const Image& u, const Image& f, const Psf& h, const RlConfig
 
 /// rl.hpp:140-179
 inline RlResult rlDeconvolve(const Image& f, const Psf& h, const RlConfig& cfg = {}) {
-    gpu_detail::validateRlInputs(f, cfg, "rlDeconvolve");
-    const std::vector<float> ff = gpu_detail::toFloat(f);
-    std::vector<float> u(ff.size());
+    // config checks here (rl.hpp:71-77), the pixel checks of rl.hpp:78-83 on
+    // the doubles inside the library, in the pass that converts them
+    gpu_detail::validateRlConfig(f, cfg, "rlDeconvolve");
+    std::vector<double> u(f.pixelCount());
     std::vector<fdg_rl_record> recs(static_cast<size_t>(cfg.iterations > 0 ? cfg.iterations : 0));
     const fdg_rl_config c = gpu_detail::toC(cfg);
-    gpu_detail::check(fdg_rl_deconvolve(gpu_detail::contextOrNull(), gpu_detail::Desc(h).get(), &c, ff.data(),
-                                        f.width(), f.height(), u.data(), recs.empty() ? nullptr : recs.data()));
-    return RlResult{gpu_detail::fromFloat(u, f.width(), f.height()), gpu_detail::toTrace(recs)};
+    gpu_detail::check(fdg_rl_deconvolve_f64(gpu_detail::contextOrNull(), gpu_detail::Desc(h).get(), &c,
+                                            f.data().data(), f.width(), f.height(), u.data(),
+                                            recs.empty() ? nullptr : recs.data()));
+    return RlResult{Image(f.width(), f.height(), std::move(u)), gpu_detail::toTrace(recs)};
 }
 
 /// rl.hpp:187-257 (+ thinStart, see the header comment)

@@ -175,6 +175,18 @@ int fdg_conv_apply_device(fdg_plan* plan, const float* d_in, float* d_out, int w
  * error the contents of u_out are unspecified. */
 int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg,
                       const float* f, int width, int height, float* u_out, fdg_rl_record* trace);
+/* The same on the reference's own pixel type (Image holds doubles,
+ * image.hpp:14-52): rlDeconvolve(const Image&, ...), rl.hpp:140-179, binds
+ * here.  The doubles become the device's fp32 planes on their way through the
+ * pinned staging chunks (a multi-threaded pass per chunk, strip by strip
+ * behind the iterations when the strip pipeline applies) and the result comes
+ * back the same way -- no float copy of the image on the host.  rl.hpp:78-83
+ * is checked on the caller's doubles in that pass (first non-finite or
+ * negative pixel in row-major order decides the message; a finite value
+ * beyond FLT_MAX is refused with "input pixel exceeds the fp32 range of the
+ * GPU path"); the verdict is read after the loop. */
+int fdg_rl_deconvolve_f64(fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl_config* cfg,
+                          const double* f, int width, int height, double* u_out, fdg_rl_record* trace);
 /* rlDeconvolve over `batch` independent width x height images stored one
  * after another (f, u_out: batch * width * height floats).  One solver runs
  * the images in chunks; with page-locked host buffers the upload of the next

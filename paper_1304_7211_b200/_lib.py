@@ -122,6 +122,8 @@ def lib():
             "fdg_conv_apply_device": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int]),
             "fdg_rl_deconvolve": (C.c_int, [vp, D, C.POINTER(RlConfigC), fp, C.c_int, C.c_int, fp,
                                             C.POINTER(RlRecordC)]),
+            "fdg_rl_deconvolve_f64": (C.c_int, [vp, D, C.POINTER(RlConfigC), C.POINTER(C.c_double), C.c_int, C.c_int,
+                                                C.POINTER(C.c_double), C.POINTER(RlRecordC)]),
             "fdg_rl_deconvolve_selective": (C.c_int, [vp, D, C.POINTER(RlConfigC), C.c_double, C.c_int,
                                                       C.c_int, u8p, u8p, fp, C.c_int, C.c_int, fp,
                                                       C.POINTER(RlRecordC)]),
@@ -308,6 +310,10 @@ def f32(a) -> np.ndarray:
 
 def fptr(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
 
 
 def u8ptr(a):

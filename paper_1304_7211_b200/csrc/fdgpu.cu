@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <chrono>
 #include <cstdlib>
+#include <cfloat>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -733,6 +734,120 @@ int d2h(Staging& S, float* h, const float* d, int pitch, int W, int H, cudaStrea
         CK(cudaEventSynchronize(S.ev[c & 1]));
         const int r0 = c * rows_per, nr = std::min(rows_per, H - r0);
         par_memcpy(h + (size_t)r0 * W, S.buf[c & 1], row * nr);
+    }
+    return FDG_OK;
+}
+
+// ---- host images in either precision.  The reference's Image holds doubles
+// (image.hpp); its pixels are converted to the device's fp32 planes on the way
+// through the pinned staging chunks (a multi-threaded pass per chunk, where a
+// float image would be copied), and rl.hpp:78-83 is checked on the caller's
+// own doubles in the same pass.
+struct HostSrc {
+    const float* f = nullptr;
+    const double* d = nullptr;
+    const void* base() const { return f ? static_cast<const void*>(f) : static_cast<const void*>(d); }
+    size_t esize() const { return f ? sizeof(float) : sizeof(double); }
+};
+struct HostDst {
+    float* f = nullptr;
+    double* d = nullptr;
+    void* base() const { return f ? static_cast<void*>(f) : static_cast<void*>(d); }
+    size_t esize() const { return f ? sizeof(float) : sizeof(double); }
+};
+// first offenders (row-major index) among the doubles converted so far
+struct F64Check {
+    std::atomic<unsigned long long> nonfinite{~0ull}, negative{~0ull}, over{~0ull};
+    void note(std::atomic<unsigned long long>& slot, unsigned long long i) {
+        unsigned long long cur = slot.load(std::memory_order_relaxed);
+        while (i < cur && !slot.compare_exchange_weak(cur, i, std::memory_order_relaxed)) {
+        }
+    }
+    // the reference's order: the first non-finite or negative pixel decides
+    // (rl.hpp:78-83); finite values beyond the fp32 range cannot be represented
+    // on the device and are refused with their own message
+    int verdict(const char* where) const {
+        const unsigned long long nf = nonfinite.load(), ng = negative.load();
+        const std::string w(where);
+        if (nf != ~0ull && nf <= ng) return set_err(FDG_EINVAL, w + ": input image has non-finite pixels");
+        if (ng != ~0ull) return set_err(FDG_EINVAL, w + ": input image must be nonnegative");
+        if (over.load() != ~0ull)
+            return set_err(FDG_EINVAL, w + ": input pixel exceeds the fp32 range of the GPU path");
+        return FDG_OK;
+    }
+};
+
+// dst[i] = (float)src[i]; offenders of rl.hpp:78-83 noted with their image index
+void par_convert_d2f(float* dst, const double* src, size_t n, unsigned long long first, F64Check* chk) {
+    const int nt = n >= (1u << 20) ? 16 : 1;
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (int t = 0; t < nt; ++t) {
+        const size_t a = n * t / nt, b = n * (t + 1) / nt;
+        bool clean = true;
+        for (size_t i = a; i < b; ++i) {
+            const double v = src[i];
+            dst[i] = static_cast<float>(v);
+            clean &= (v >= 0.0) & (v <= static_cast<double>(FLT_MAX));  // false for NaN, inf, negatives
+        }
+        if (!clean && chk)
+            for (size_t i = a; i < b; ++i) {
+                const double v = src[i];
+                if (!std::isfinite(v)) chk->note(chk->nonfinite, first + i);
+                else if (v < 0.0) chk->note(chk->negative, first + i);
+                else if (v > static_cast<double>(FLT_MAX)) chk->note(chk->over, first + i);
+            }
+    }
+}
+
+void par_convert_f2d(double* dst, const float* src, size_t n) {
+    const int nt = n >= (1u << 20) ? 16 : 1;
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (int t = 0; t < nt; ++t) {
+        const size_t a = n * t / nt, b = n * (t + 1) / nt;
+        for (size_t i = a; i < b; ++i) dst[i] = static_cast<double>(src[i]);
+    }
+}
+
+// rows [r0, r0 + nr) of a W-wide host image -> device rows (d points at row r0)
+int h2d_rows(Staging& S, float* d, int pitch, const HostSrc& src, int r0, int W, int nr, cudaStream_t st,
+             F64Check* chk) {
+    if (src.f) return h2d(S, d, pitch, src.f + (size_t)r0 * W, W, nr, st);
+    const size_t row = (size_t)W * 4;
+    CK(S.init());
+    const int rows_per = (int)std::max<size_t>(1, Staging::CHUNK / row);
+    for (int q0 = 0, k = 0; q0 < nr; q0 += rows_per, k ^= 1) {
+        const int n = std::min(rows_per, nr - q0);
+        CK(cudaEventSynchronize(S.ev[k]));  // the previous DMA out of this chunk is done
+        const size_t first = (size_t)(r0 + q0) * W;
+        par_convert_d2f(S.buf[k], src.d + first, (size_t)n * W, first, chk);
+        CK(cudaMemcpy2DAsync(d + (size_t)q0 * pitch, (size_t)pitch * 4, S.buf[k], row, row, n, cudaMemcpyHostToDevice,
+                             st));
+        CK(cudaEventRecord(S.ev[k], st));
+    }
+    return FDG_OK;
+}
+
+// device rows -> rows [r0, r0 + nr) of a W-wide host image (d points at row r0); returns when they are there
+int d2h_rows(Staging& S, const HostDst& dst, int r0, const float* d, int pitch, int W, int nr, cudaStream_t st) {
+    if (dst.f) return d2h(S, dst.f + (size_t)r0 * W, d, pitch, W, nr, st);
+    const size_t row = (size_t)W * 4;
+    CK(S.init());
+    const int rows_per = (int)std::max<size_t>(1, Staging::CHUNK / row);
+    const int nchunk = (nr + rows_per - 1) / rows_per;
+    auto issue = [&](int c) -> cudaError_t {
+        const int q0 = c * rows_per, n = std::min(rows_per, nr - q0);
+        cudaError_t e = cudaStreamWaitEvent(st, S.ev[c & 1], 0);  // the chunk's previous DMA has drained
+        if (e != cudaSuccess) return e;
+        e = cudaMemcpy2DAsync(S.buf[c & 1], row, d + (size_t)q0 * pitch, (size_t)pitch * 4, row, n,
+                              cudaMemcpyDeviceToHost, st);
+        return e == cudaSuccess ? cudaEventRecord(S.ev[c & 1], st) : e;
+    };
+    if (nchunk > 0) CK(issue(0));
+    for (int c = 0; c < nchunk; ++c) {
+        if (c + 1 < nchunk) CK(issue(c + 1));  // next DMA (other chunk) overlaps this chunk's conversion
+        CK(cudaEventSynchronize(S.ev[c & 1]));
+        const int q0 = c * rows_per, n = std::min(rows_per, nr - q0);
+        par_convert_f2d(dst.d + (size_t)(r0 + q0) * W, S.buf[c & 1], (size_t)n * W);
     }
     return FDG_OK;
 }
@@ -1541,22 +1656,22 @@ std::vector<int> pipe_strips(int H, int D, int iters) {
 // option "pipeline": 0 off, 1 large images only (>= 48 Mpx, >= 4096 rows: the
 // strips must be tall enough to keep every SM busy), 2 whenever the engine and
 // the buffers allow (tests)
-bool pipe_applies(const fdg_solver* sv, int W, int H, int iters, const float* f, const float* u_out) {
+bool pipe_applies(const fdg_solver* sv, int W, int H, int iters, const HostSrc& f, const HostDst& u_out) {
     const int mode = g_pipeline.load();
     if (mode < 1 || iters < 1 || sv->batch != 1) return false;
     if (!use_fused(sv->fwd.get()) || !fused_halo_ok(W) || use_rowres(sv->fwd.get(), W)) return false;
     if (mode == 1 && ((long long)W * H < (48ll << 20) || H < 4096)) return false;
     // in-place calls (the result over the input): downloads would land in
     // rows whose upload may still be queued
-    const char *fa = reinterpret_cast<const char*>(f), *ua = reinterpret_cast<const char*>(u_out);
-    const size_t bytes = (size_t)W * H * sizeof(float);
-    return !(fa < ua + bytes && ua < fa + bytes);
+    const char *fa = static_cast<const char*>(f.base()), *ua = static_cast<const char*>(u_out.base());
+    const size_t px = (size_t)W * H;
+    return !(fa < ua + px * u_out.esize() && ua < fa + px * f.esize());
 }
 
 // The whole call: uploads, validation, iterations, downloads, trace.  mc / nf
 // / sec: per iteration (sec = the iteration's launches summed over strips).
-int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, float* df, float* du, int pitch,
-                 std::vector<float>* mc, std::vector<int>* nf, std::vector<double>* sec) {
+int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const HostSrc& f, const HostDst& u_out, F64Check* chk, float* df,
+                 float* du, int pitch, std::vector<float>* mc, std::vector<int>* nf, std::vector<double>* sec) {
     const int W = sv->W, H = sv->H, K = sv->cfg.iterations;
     const int D = 2 * (sv->fwd->dev.my / 2);
     const std::vector<int> a = pipe_strips(H, D, K);
@@ -1606,14 +1721,14 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, flo
     // copy per chunk, which occupies this thread), so strip s + 1 is staged
     // right after strip s's launches are queued, while the device works on them;
     // likewise a pageable result is fetched (d2h, blocking) one strip late.
-    const bool pin_in = !pageable(f), pin_out = !pageable(u_out);
+    const bool pin_in = f.f && !pageable(f.f), pin_out = u_out.f && !pageable(u_out.f);
     CK(cudaEventRecord(pc->ev[2 * n], comp));
     CK(cudaStreamWaitEvent(pc->cin, pc->ev[2 * n], 0));
     std::vector<int> c(n + 1, 0), flo(n, 0), fhi(n, 0);
     for (int s = 0; s < n; ++s) c[s + 1] = s == n - 1 ? H : std::max(c[s], std::min(H, a[s + 1] + D));
     auto upload = [&](int s) -> int {
         if (c[s + 1] > c[s])
-            if (int st = h2d(ctx->stg, df + (size_t)c[s] * pitch, pitch, f + (size_t)c[s] * W, W, c[s + 1] - c[s], pc->cin))
+            if (int st = h2d_rows(ctx->stg, df + (size_t)c[s] * pitch, pitch, f, c[s], W, c[s + 1] - c[s], pc->cin, chk))
                 return st;
         CK(cudaEventRecord(pc->ev[2 * s], pc->cin));
         if (dbg) CK(cudaEventRecord(tev[3 * s], pc->cin));
@@ -1622,8 +1737,8 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, flo
     auto download = [&](int s) -> int {  // the strip's final rows, after its last launch
         if (fhi[s] > flo[s]) {
             CK(cudaStreamWaitEvent(pc->cout_, pc->ev[2 * s + 1], 0));
-            if (int st = d2h(ctx->stg, u_out + (size_t)flo[s] * W, du + (size_t)flo[s] * pitch, pitch, W,
-                             fhi[s] - flo[s], pc->cout_))
+            if (int st = d2h_rows(ctx->stg, u_out, flo[s], du + (size_t)flo[s] * pitch, pitch, W, fhi[s] - flo[s],
+                                  pc->cout_))
                 return st;
         }
         if (dbg) CK(cudaEventRecord(tev[3 * s + 2], pc->cout_));
@@ -1666,7 +1781,7 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, flo
         // result pages, bring finished rows home
         if (!pin_in && s + 1 < n)
             if (int st = upload(s + 1)) return st;
-        if (s == std::min(1, n - 1)) prefault(u_out, (size_t)W * H * sizeof(float));
+        if (s == std::min(1, n - 1)) prefault(u_out.base(), (size_t)W * H * u_out.esize());
         if (pin_out) {
             if (int st = download(s)) return st;
         } else if (s >= 1) {
@@ -1707,14 +1822,25 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const float* f, float* u_out, flo
 }
 }  // namespace
 
-extern "C" {
-int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, const float* f, int W,
-                      int H, float* u_out, fdg_rl_record* trace) {
+namespace {
+// rlDeconvolve (rl.hpp:140-179) on a host image of either precision
+int rl_deconvolve_impl(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, const HostSrc& f, int W,
+                       int H, const HostDst& u_out, fdg_rl_record* trace) {
     PhaseTimer pt;
-    int st = validate_cfg(f, W, H, cfg, "rlDeconvolve");
+    int st = validate_cfg(static_cast<const float*>(f.base()), W, H, cfg, "rlDeconvolve");
     if (st) return st;
+    if (!u_out.base()) return set_err(FDG_EINVAL, "rlDeconvolve: null output");
+    F64Check chk64;
+    F64Check* chk = f.d ? &chk64 : nullptr;
     if (!ctx) {  // no device: validate on the host so the reference's errors still surface
-        if ((st = validate_rl(f, W, H, cfg, "rlDeconvolve"))) return st;
+        if (f.f) {
+            if ((st = validate_rl(f.f, W, H, cfg, "rlDeconvolve"))) return st;
+        } else {
+            std::vector<float> tmp(std::min<size_t>((size_t)W * H, 1u << 20));
+            for (size_t o = 0; o < (size_t)W * H; o += tmp.size())
+                par_convert_d2f(tmp.data(), f.d + o, std::min(tmp.size(), (size_t)W * H - o), o, chk);
+            if ((st = chk->verdict("rlDeconvolve"))) return st;
+        }
         Entry en;
         return enter(ctx, en);
     }
@@ -1766,8 +1892,9 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
         std::vector<float> mc;
         std::vector<int> nf;
         std::vector<double> sec;
-        if ((st = rl_pipelined(ctx, sv, f, u_out, df, du, pitch, &mc, &nf, &sec))) return st;
+        if ((st = rl_pipelined(ctx, sv, f, u_out, chk, df, du, pitch, &mc, &nf, &sec))) return st;
         pt.mark("pipelined");
+        if (chk && (st = chk->verdict("rlDeconvolve"))) return st;  // the caller's doubles decide
         const unsigned long long nf0 = ctx->h_bad[0], neg0 = ctx->h_bad[1];
         if (nf0 != ~0ull && nf0 <= neg0) return set_err(FDG_EINVAL, "rlDeconvolve: input image has non-finite pixels");
         if (neg0 != ~0ull) return set_err(FDG_EINVAL, "rlDeconvolve: input image must be nonnegative");
@@ -1777,7 +1904,8 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
         }
         return FDG_OK;
     }
-    if ((st = h2d(ctx->stg, df, pitch, f, W, H, s))) return st;
+    if ((st = h2d_rows(ctx->stg, df, pitch, f, 0, W, H, s, chk))) return st;
+    if (chk && (st = chk->verdict("rlDeconvolve"))) return st;  // the whole image has been looked at
     if (!sv && (st = validate_device(ctx, df, W, H, pitch, "rlDeconvolve"))) return st;
     pt.mark("h2d+validate");
     if (sv) {
@@ -1790,12 +1918,12 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
         CK(cudaMemcpyAsync(ctx->h_bad, ctx->first_bad.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         if ((st = solver_reset_trace(sv))) return st;
         if ((st = solver_run(sv, df, du, pitch, 0, iters))) return st;
-        prefault(u_out, (size_t)W * H * sizeof(float));
+        prefault(u_out.base(), (size_t)W * H * u_out.esize());
         if (pt.on) {
             CK(cudaStreamSynchronize(s));
             pt.mark("iterate(graph)");
         }
-        if ((st = d2h(ctx->stg, u_out, du, pitch, W, H, s))) return st;
+        if ((st = d2h_rows(ctx->stg, u_out, 0, du, pitch, W, H, s))) return st;
         std::vector<float> mc;
         std::vector<int> nf;
         std::vector<double> sec;
@@ -1852,12 +1980,12 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     }
     // While the device iterates, fault in the (pageable) output pages on the
     // host so the final D2H does not pay first-touch page faults.
-    prefault(u_out, (size_t)W * H * sizeof(float));
+    prefault(u_out.base(), (size_t)W * H * u_out.esize());
     if (pt.on) {
         CK(cudaStreamSynchronize(s));
         pt.mark("iterate");
     }
-    if ((st = d2h(ctx->stg, u_out, du, pitch, W, H, s))) return st;
+    if ((st = d2h_rows(ctx->stg, u_out, 0, du, pitch, W, H, s))) return st;
     std::vector<unsigned> hmc(iters + 1);
     std::vector<int> hnf(iters + 1);
     std::vector<unsigned long long> hts(iters + 2), hdur(rowres ? iters : 0);
@@ -1877,6 +2005,26 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
         }
     }
     return FDG_OK;
+}
+}  // namespace
+
+extern "C" {
+int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, const float* f, int W,
+                      int H, float* u_out, fdg_rl_record* trace) {
+    HostSrc src;
+    src.f = f;
+    HostDst dst;
+    dst.f = u_out;
+    return rl_deconvolve_impl(ctx, desc, cfg, src, W, H, dst, trace);
+}
+
+int fdg_rl_deconvolve_f64(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, const double* f, int W,
+                          int H, double* u_out, fdg_rl_record* trace) {
+    HostSrc src;
+    src.d = f;
+    HostDst dst;
+    dst.d = u_out;
+    return rl_deconvolve_impl(ctx, desc, cfg, src, W, H, dst, trace);
 }
 
 int fdg_rl_step(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, const float* u, const float* f,

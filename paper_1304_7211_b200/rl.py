@@ -89,15 +89,20 @@ def _image(f) -> np.ndarray:
     return a
 
 
-def _validate(a: np.ndarray, cfg: RlConfig, where: str):
-    """rl.hpp:71-84 in the reference's order (config first, then pixels) on
-    the caller's own values; float32 input is validated on the device."""
+def _validate_cfg(a: np.ndarray, cfg: RlConfig, where: str):
+    """rl.hpp:71-77: the checks that come before the pixels"""
     if a.size == 0:
         raise _lib.FdgInvalidArgument(f"{where}: empty input image")
     if cfg.iterations < 0:
         raise _lib.FdgInvalidArgument(f"{where}: iterations must be >= 0")
     if not (cfg.epsilonDiv > 0.0):
         raise _lib.FdgInvalidArgument(f"{where}: epsilonDiv must be positive")
+
+
+def _validate(a: np.ndarray, cfg: RlConfig, where: str):
+    """rl.hpp:71-84 in the reference's order (config first, then pixels) on
+    the caller's own values; float32 input is validated on the device."""
+    _validate_cfg(a, cfg, where)
     _lib.validate_image(a, where)
 
 
@@ -120,11 +125,31 @@ def _out(a, u32):
 
 def rlDeconvolve(f, h, cfg: RlConfig = RlConfig(), ctx: Optional[Context] = None,
                  out: Optional[np.ndarray] = None) -> RlResult:
-    """Standard RL from u0 = f (rl.hpp:140-179).  ``out``: optional float32
-    C-contiguous (H, W) array that receives the result (e.g. page-locked
-    memory: the device -> host copy then runs at full DMA speed instead of
-    through the pinned staging chunks)."""
+    """Standard RL from u0 = f (rl.hpp:140-179).  ``out``: optional
+    C-contiguous (H, W) array of the image's dtype that receives the result
+    (e.g. page-locked memory: the device -> host copy then runs at full DMA
+    speed instead of through the pinned staging chunks).  float64 images (the
+    reference's pixel type) go to fdg_rl_deconvolve_f64: converted and checked
+    (rl.hpp:78-83, on the doubles) chunk by chunk on their way to the device,
+    the result converted back the same way."""
     a = _image(f)
+    n = max(cfg.iterations, 0)
+    recs = (RlRecordC * max(n, 1))()
+    c = cfg.c()
+    if a.dtype == np.float64 and a.size:
+        _validate_cfg(a, cfg, "rlDeconvolve")
+        src = np.ascontiguousarray(a)
+        hh, w = src.shape
+        if out is not None:
+            if out.dtype != np.float64 or out.shape != src.shape or not out.flags.c_contiguous:
+                raise _lib.FdgInvalidArgument(
+                    "rlDeconvolve: out must be a C-contiguous float64 array of the image's shape")
+            u = out
+        else:
+            u = np.empty_like(src)
+        check(lib().fdg_rl_deconvolve_f64(Context.handle_or_null(ctx), Desc(h).ref, C.byref(c), _lib.dptr(src), w, hh,
+                                          _lib.dptr(u), recs))
+        return RlResult(u, _trace(recs, n))
     _validate(a, cfg, "rlDeconvolve")
     src = f32(a)
     hh, w = src.shape if src.size else (0, 0)
@@ -134,9 +159,6 @@ def rlDeconvolve(f, h, cfg: RlConfig = RlConfig(), ctx: Optional[Context] = None
         u = out
     else:
         u = np.empty_like(src)
-    n = max(cfg.iterations, 0)
-    recs = (RlRecordC * max(n, 1))()
-    c = cfg.c()
     check(lib().fdg_rl_deconvolve(Context.handle_or_null(ctx), Desc(h).ref, C.byref(c), fptr(src), w, hh, fptr(u), recs))
     return RlResult(_out(a, u), _trace(recs, n))
 

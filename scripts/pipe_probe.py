@@ -16,17 +16,18 @@ size = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 4
 pinned = (sys.argv[4] if len(sys.argv) > 4 else "pinned") == "pinned"
+f64 = len(sys.argv) > 5 and sys.argv[5] == "f64"  # the reference's pixel type (pageable doubles)
 cfg = W.CONFIGS["cfg4"]
 ctx = Context(0)
 rng = np.random.default_rng(4)
 f = (0.2 + 0.8 * rng.random((size, size), dtype=np.float32))
 f[size // 3: size // 3 + 900, :] *= 0.25  # structure, so iterations move
 psf = W.make_psf(cfg.psf)
-fp = torch.from_numpy(f).pin_memory().numpy() if pinned else f
+fp = f.astype(np.float64) if f64 else (torch.from_numpy(f).pin_memory().numpy() if pinned else f)
 outs = {}
 for mode in (0, 1):
     lib().fdg_set_option(b"pipeline", mode)
-    up = torch.empty(f.shape, dtype=torch.float32).pin_memory().numpy() if pinned else np.empty_like(f)
+    up = np.empty_like(fp) if f64 else (torch.empty(f.shape, dtype=torch.float32).pin_memory().numpy() if pinned else np.empty_like(f))
     rc = RlConfig(iterations=iters, op=OperatorKind.Box2dSliding)
     for _ in range(2):
         res = rlDeconvolve(fp, psf, rc, ctx=ctx, out=up)
@@ -39,7 +40,7 @@ for mode in (0, 1):
     res = rlDeconvolve(fp, psf, rc, ctx=ctx, out=up)
     print(f"  repeat call bit-identical: {np.array_equal(outs[mode], up)}")
     tr = res.trace.records
-    print(f"{'pinned' if pinned else 'pageable'} pipeline={mode}: {dt * 1e3:.2f} ms per call, {size * size * iters / dt / 1e6:.0f} Mpx*it/s e2e; "
+    print(f"{'float64' if f64 else 'pinned' if pinned else 'pageable'} pipeline={mode}: {dt * 1e3:.2f} ms per call, {size * size * iters / dt / 1e6:.0f} Mpx*it/s e2e; "
           f"trace maxc[0]={tr[0].maxAbsChange:.4g} maxc[-1]={tr[-1].maxAbsChange:.4g} "
           f"sum(sec)={sum(r.seconds for r in tr) * 1e3:.2f} ms", flush=True)
 d = np.abs(outs[0] - outs[1])
