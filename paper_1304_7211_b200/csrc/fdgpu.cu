@@ -1726,6 +1726,8 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const HostSrc& f, const HostDst& 
     CK(cudaStreamWaitEvent(pc->cin, pc->ev[2 * n], 0));
     std::vector<int> c(n + 1, 0), flo(n, 0), fhi(n, 0);
     for (int s = 0; s < n; ++s) c[s + 1] = s == n - 1 ? H : std::max(c[s], std::min(H, a[s + 1] + D));
+    // (a pageable result's pages are first touched by the staged downloads'
+    // own multi-threaded copy / conversion passes, behind the iterations)
     auto upload = [&](int s) -> int {
         if (c[s + 1] > c[s])
             if (int st = h2d_rows(ctx->stg, df + (size_t)c[s] * pitch, pitch, f, c[s], W, c[s + 1] - c[s], pc->cin, chk))
@@ -1781,7 +1783,6 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const HostSrc& f, const HostDst& 
         // result pages, bring finished rows home
         if (!pin_in && s + 1 < n)
             if (int st = upload(s + 1)) return st;
-        if (s == std::min(1, n - 1)) prefault(u_out.base(), (size_t)W * H * u_out.esize());
         if (pin_out) {
             if (int st = download(s)) return st;
         } else if (s >= 1) {

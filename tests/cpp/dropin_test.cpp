@@ -6,6 +6,8 @@
 // against the CPU oracle (oracle/liboracle.so, test infrastructure).
 //
 // usage: dropin_test [--cpu-only]     exit status = number of failed checks
+//        dropin_test --time W H ITERS   wall time of rlDeconvolve(Image) through the drop-in
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -329,7 +331,33 @@ static void deviceChecks() {
     }
 }
 
+// --time W H ITERS: wall time of the reference-API call rlDeconvolve(const
+// Image&, ...) (doubles in, doubles out, 15 x 15 box) through the drop-in
+static int timeDropIn(int w, int h, int iters) {
+    Image f(w, h, 0.5);
+    std::mt19937 rng(4);
+    std::uniform_real_distribution<double> d(0.2, 1.0);
+    for (int y = 0; y < h; y += 7)
+        for (int x = 0; x < w; ++x) f.row(y)[x] = d(rng);
+    const Psf psf = makeBoxPsf(15, 15);
+    RlConfig cfg;
+    cfg.iterations = iters;
+    cfg.op = OperatorKind::Box2dSliding;
+    for (int rep = 0; rep < 4; ++rep) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const RlResult r = rlDeconvolve(f, psf, cfg);
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        std::printf("rlDeconvolve(Image %dx%d, box 15x15, %d iterations): %.1f ms per call, %.0f Mpx*it/s "
+                    "(device %.1f ms; u[1][1] = %.6f)\n",
+                    w, h, iters, ms, (double)w * h * iters / ms / 1e3, r.trace.totalSeconds() * 1e3,
+                    r.image.row(1)[1]);
+    }
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    if (argc > 4 && std::string(argv[1]) == "--time")
+        return timeDropIn(std::atoi(argv[2]), std::atoi(argv[3]), std::atoi(argv[4]));
     const bool cpu_only = argc > 1 && std::string(argv[1]) == "--cpu-only";
     hostChecks();
     if (!cpu_only) deviceChecks();
