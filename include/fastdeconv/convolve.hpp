@@ -15,6 +15,7 @@
 // numbers as with the CPU operators.
 #pragma once
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
@@ -25,6 +26,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <thread>
 #include <variant>
 #include <vector>
 
@@ -145,12 +147,36 @@ private:
     std::vector<double> w_;
 };
 
+/// [0, n) split over a few threads for the pixel-type conversions of large
+/// images (the device works in fp32, Image holds doubles)
+template <typename F>
+inline void parallelRanges(std::size_t n, F&& body) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const unsigned nt = n >= (std::size_t(1) << 22) ? std::min(16u, hw ? hw : 1u) : 1u;
+    if (nt <= 1) {
+        body(std::size_t(0), n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) th.emplace_back([&body, n, t, nt] { body(n * t / nt, n * (t + 1) / nt); });
+    for (std::thread& x : th) x.join();
+}
+
 inline std::vector<float> toFloat(const Image& img) {
-    return std::vector<float>(img.data().begin(), img.data().end());
+    const std::vector<double>& d = img.data();
+    std::vector<float> out(d.size());
+    parallelRanges(d.size(), [&](std::size_t a, std::size_t b) {
+        for (std::size_t i = a; i < b; ++i) out[i] = static_cast<float>(d[i]);
+    });
+    return out;
 }
 
 inline Image fromFloat(const std::vector<float>& v, int w, int h) {
-    return Image(w, h, std::vector<double>(v.begin(), v.end()));
+    std::vector<double> out(v.size());
+    parallelRanges(v.size(), [&](std::size_t a, std::size_t b) {
+        for (std::size_t i = a; i < b; ++i) out[i] = static_cast<double>(v[i]);
+    });
+    return Image(w, h, std::move(out));
 }
 
 }  // namespace gpu_detail
