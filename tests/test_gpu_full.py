@@ -133,8 +133,25 @@ def test_cfg4_full_16384_fused(oq):
     solver = RlSolver(d["psf"], RlConfig(iterations=cfg.iterations, op=K.Box2dSliding), cfg.width, cfg.height)
     assert solver.engine() == "fused"
     del solver
-    res = rlDeconvolve(d["f"], d["psf"], RlConfig(iterations=cfg.iterations, op=K.Box2dSliding))
+    # both schedules of the host-buffer call: upload -> whole-image launches ->
+    # download, and the time-skewed strip pipeline (the default at this size)
+    from paper_1304_7211_b200 import _lib
+    from paper_1304_7211_b200._lib import Context
+    ctx = Context(0)
+    rc = RlConfig(iterations=cfg.iterations, op=K.Box2dSliding)
+    prev = _lib.lib().fdg_set_option(b"pipeline", 0)
+    try:
+        res = rlDeconvolve(d["f"], d["psf"], rc, ctx=ctx)
+    finally:
+        _lib.lib().fdg_set_option(b"pipeline", prev)
+    assert ctx.last_schedule() == 0
     _check("cfg4", res.image, d["ref"], d["g"])
+    gm = np.array([r.maxAbsChange for r in res.trace.records])
+    np.testing.assert_allclose(gm, d["mc"], rtol=2e-2, atol=1e-6)
+    del res
+    res = rlDeconvolve(d["f"], d["psf"], rc, ctx=ctx)
+    assert ctx.last_schedule() >= 2
+    _check("cfg4 (strip pipeline)", res.image, d["ref"], d["g"])
     gm = np.array([r.maxAbsChange for r in res.trace.records])
     np.testing.assert_allclose(gm, d["mc"], rtol=2e-2, atol=1e-6)
 
