@@ -1,5 +1,5 @@
 // kernels_fused.cu -- one launch per Richardson-Lucy iteration for centred
-// square boxes 9 x 9 / 15 x 15 / 17 x 17 (Box2d*, config 4 = 15 x 15): both
+// square boxes 3 x 3 ... 17 x 17 (Box2d*, config 4 = 15 x 15): both
 // convolutions, the quotient and the multiplicative update fused, q never
 // leaving the SM.
 //
@@ -803,9 +803,9 @@ std::atomic<int> g_fused{getenv("FDG_FUSED") ? atoi(getenv("FDG_FUSED")) : 1};
 void set_fused_mode(int v) { g_fused.store(v); }
 int fused_mode() { return g_fused.load(); }
 
-// centred square boxes 9 x 9, 15 x 15 (config 4) and 17 x 17
+// centred square boxes 3 x 3 ... 17 x 17 (config 4 = 15 x 15)
 bool fused_supported(int mx, int my, int min_dx, int min_dy) {
-    return g_fused.load() == 1 && mx == my && (mx == 9 || mx == 15 || mx == 17) && min_dx == -(mx / 2) &&
+    return g_fused.load() == 1 && mx == my && (mx & 1) && mx >= 3 && mx <= 17 && min_dx == -(mx / 2) &&
            min_dy == -(my / 2);
 }
 
@@ -855,8 +855,17 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
     a.nanflag = nanflag;
     a.tend = tend;
     static const int variant = getenv("FDG_FUSED_V") ? atoi(getenv("FDG_FUSED_V")) : 0;
-    if (rx == 4) return launch_t<4, 4, 128, 2, 12, 8, 2, true>(a, st);  // 9 x 9
-    if (rx == 8) return launch_t<8, 8, 128, 2, 12, 8, 2, true>(a, st);  // 17 x 17
+    switch (rx) {  // every radius but config 4's: the generic window sums (hsumx4)
+        case 1: return launch_t<1, 1, 128, 2, 12, 8, 2, true>(a, st);  // 3 x 3
+        case 2: return launch_t<2, 2, 128, 2, 12, 8, 2, true>(a, st);
+        case 3: return launch_t<3, 3, 128, 2, 12, 8, 2, true>(a, st);
+        case 4: return launch_t<4, 4, 128, 2, 12, 8, 2, true>(a, st);  // 9 x 9
+        case 5: return launch_t<5, 5, 128, 2, 12, 8, 2, true>(a, st);
+        case 6: return launch_t<6, 6, 128, 2, 12, 8, 2, true>(a, st);
+        case 8: return launch_t<8, 8, 128, 2, 12, 8, 2, true>(a, st);  // 17 x 17
+        case 7: break;
+        default: return cudaErrorInvalidValue;
+    }
     switch (variant) {
         case 1: return launch_t<7, 7, 128, 2, 12, 8, 2, false>(a, st);  // no L2 cache hints
         default: return launch_t<7, 7, 128, 2, 12, 8, 2, true>(a, st);

@@ -131,7 +131,7 @@ def test_fused_iterate_rejects_non_fused_solver():
     from paper_1304_7211_b200 import RlSolver
     from paper_1304_7211_b200._lib import FdgInvalidArgument
     from paper_1304_7211_b200.psf import makeBoxPsf
-    s = RlSolver(makeBoxPsf(5, 5), RlConfig(iterations=2, op=K.Box2dSliding), 64, 64)
+    s = RlSolver(makeBoxPsf(5, 3), RlConfig(iterations=2, op=K.Box2dSliding), 64, 64)
     assert s.engine() != "fused"
     with pytest.raises(FdgInvalidArgument):
         s.iterate(1, 2, 3, 64, 64 * 64, 0, 64, 0, 63, 0)
@@ -225,12 +225,12 @@ def test_rowres_column_split_edges(w):
     assert W.max_rel(res.image, ref) <= 1e-5
 
 
-@pytest.mark.parametrize("m", [9, 17])
+@pytest.mark.parametrize("m", [3, 5, 7, 9, 11, 13, 17])
 @pytest.mark.parametrize("w,h,it", [(1024, 768, 12), (37, 23, 5), (5, 3, 4), (513, 129, 7), (2050, 300, 2),
                                     (600, 1, 3), (8192, 20, 3)])
 def test_fused_other_boxes_match_oracle(m, w, h, it):
-    """The one-launch iteration for the centred 9 x 9 and 17 x 17 boxes
-    (generic window sums, 9- / 17-row vertical rings)."""
+    """The one-launch iteration for every other centred odd square box up to
+    17 x 17 (generic window sums, m-row vertical rings)."""
     from paper_1304_7211_b200 import RlSolver
     from paper_1304_7211_b200.psf import makeBoxPsf
     psf = makeBoxPsf(m, m)

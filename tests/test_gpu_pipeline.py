@@ -86,7 +86,7 @@ def test_pipelined_matches_oracle(w, h, it, strips):
     assert all(r.seconds > 0 for r in res.trace.records)
 
 
-@pytest.mark.parametrize("m", [9, 17])
+@pytest.mark.parametrize("m", [3, 5, 9, 17])
 def test_pipelined_other_boxes(m):
     psf = P.makeBoxPsf(m, m)
     f, _ = _input(1024, 640, m, psf)
