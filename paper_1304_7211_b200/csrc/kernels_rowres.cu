@@ -260,11 +260,27 @@ cudaError_t launch_m(const RowResArgs& a, int threads, size_t smem, int blocks, 
 
 }  // namespace
 
+// anchor-centred horizontal lines of 5 .. 31 px (8 columns per thread -- rows
+// wider than 1024 px -- need a window of at least 9)
 bool rowres_supported(int mx, int my, int min_dx, int min_dy, int W) {
     // one row per <= 256-thread CTA: W <= 256 x 8 columns
-    return my == 1 && min_dy == 0 && min_dx == -(mx / 2) && (mx == 15 || mx == 31 || mx == 9 || mx == 17) &&
-           W >= 1 && W <= 2048;
+    return my == 1 && min_dy == 0 && min_dx == -(mx / 2) && mx <= 31 && mx >= (W <= 1024 ? 5 : 9) && W >= 1 &&
+           W <= 2048;
 }
+
+namespace {
+// the instantiation for line length mx, M = 5 .. 31
+template <int M>
+cudaError_t launch_len(int mx, int PT, const RowResArgs& a, int threads, size_t smem, int blocks, cudaStream_t st) {
+    if (mx == M) {
+        if (PT == 4) return launch_m<M, 4>(a, threads, smem, blocks, st);
+        if constexpr (M >= 9) return launch_m<M, 8>(a, threads, smem, blocks, st);
+        return cudaErrorInvalidValue;
+    }
+    if constexpr (M < 31) return launch_len<M + 1>(mx, PT, a, threads, smem, blocks, st);
+    return cudaErrorInvalidValue;
+}
+}  // namespace
 
 cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float* u, int pitch, int W, int H,
                           int batch, long long bstride, int iters, float eps, int clamp, unsigned* maxchange,
@@ -311,17 +327,7 @@ cudaError_t launch_rowres(int mx, int min_dx, float inv_m, const float* f, float
                         sizeof(unsigned long long) * iters;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     const int blocks = (a.rows_total + rows_per_cta - 1) / rows_per_cta;
-    switch (mx * 16 + PT) {
-        case 9 * 16 + 4: return launch_m<9, 4>(a, threads, smem, blocks, st);
-        case 15 * 16 + 4: return launch_m<15, 4>(a, threads, smem, blocks, st);
-        case 17 * 16 + 4: return launch_m<17, 4>(a, threads, smem, blocks, st);
-        case 31 * 16 + 4: return launch_m<31, 4>(a, threads, smem, blocks, st);
-        case 9 * 16 + 8: return launch_m<9, 8>(a, threads, smem, blocks, st);
-        case 15 * 16 + 8: return launch_m<15, 8>(a, threads, smem, blocks, st);
-        case 17 * 16 + 8: return launch_m<17, 8>(a, threads, smem, blocks, st);
-        case 31 * 16 + 8: return launch_m<31, 8>(a, threads, smem, blocks, st);
-    }
-    return cudaErrorInvalidValue;
+    return launch_len<5>(mx, PT, a, threads, smem, blocks, st);
 }
 
 }  // namespace fdg

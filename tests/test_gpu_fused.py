@@ -253,3 +253,22 @@ def test_fused_repeat_calls_are_bit_identical():
     a = rlDeconvolve(f, psf, cfg).image
     for _ in range(3):
         assert np.array_equal(a, rlDeconvolve(f, psf, cfg).image)
+
+
+@pytest.mark.parametrize("m", [5, 6, 7, 8, 9, 10, 12, 21, 22, 30, 31])
+@pytest.mark.parametrize("w,h", [(700, 9), (3, 4), (1500, 5)])
+def test_rowres_every_line_length(m, w, h):
+    """The row-resident engine for every anchor-centred horizontal line of
+    5 .. 31 px (odd and even lengths; rows wider than 1024 px use 8 columns
+    per thread and need a window of at least 9), against the oracle."""
+    from paper_1304_7211_b200 import RlSolver
+    from paper_1304_7211_b200.psf import makeLinePsf
+    rng = np.random.default_rng(m * 100 + w)
+    f = (rng.random((h, w)) * 0.9 + 0.1).astype(np.float32)
+    psf = makeLinePsf(m)
+    expect = "rowres" if (w <= 1024 or m >= 9) else "box"
+    assert RlSolver(psf, RlConfig(iterations=9, op=K.Box1dSliding), w, h).engine() == expect
+    res = rlDeconvolve(f, psf, RlConfig(iterations=9, op=K.Box1dSliding))
+    ref, mc, _ = O.rl_deconvolve(f.astype(np.float64), psf, 9, O.BOX1D_SLIDING)
+    assert W.max_rel(res.image, ref) <= 1e-5
+    np.testing.assert_allclose([r.maxAbsChange for r in res.trace.records], mc, rtol=1e-3, atol=1e-6)
