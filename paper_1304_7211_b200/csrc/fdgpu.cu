@@ -2019,6 +2019,19 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     return rl_deconvolve_impl(ctx, desc, cfg, src, W, H, dst, trace);
 }
 
+// The strip pipeline's layout for an image of `height` rows, `shift` rows of
+// dependency per iteration (2 x the box's vertical radius) and `iterations`
+// iterations: the strips' first rows at iteration 0 (bounds[0] = 0; a value
+// beyond height = a strip born later, see pipe_strips).  Returns the number of
+// strips (bounds holds min(n, cap) of them).  Host only: lets a test check the
+// schedule's dependences without a device.
+int fdg_pipeline_layout(int height, int shift, int iterations, int* bounds, int cap) {
+    if (height < 1 || shift < 0 || iterations < 0 || (cap > 0 && !bounds)) return 0;
+    const std::vector<int> a = pipe_strips(height, shift, iterations);
+    for (int i = 0; i < (int)a.size() && i < cap; ++i) bounds[i] = a[i];
+    return (int)a.size();
+}
+
 int fdg_rl_deconvolve_f64(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_config* cfg, const double* f, int W,
                           int H, double* u_out, fdg_rl_record* trace) {
     HostSrc src;
