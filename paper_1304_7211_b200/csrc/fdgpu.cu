@@ -1779,8 +1779,8 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const HostSrc& f, const HostDst& 
         }
         CK(cudaEventRecord(pc->ev[2 * s + 1], comp));
         if (dbg) CK(cudaEventRecord(tev[3 * s + 1], comp));
-        // the device is busy with strip s: stage the next upload, fault in the
-        // result pages, bring finished rows home
+        // the device is busy with strip s: stage the next upload, bring
+        // finished rows home
         if (!pin_in && s + 1 < n)
             if (int st = upload(s + 1)) return st;
         if (pin_out) {
