@@ -103,8 +103,9 @@ int fdg_get_device(int* device);
  *            kernel, 2 = marching kernel.
  *   "pipeline": fdg_rl_deconvolve with the fused engine runs as time-skewed
  *            row strips whose uploads / downloads (pageable buffers: staged)
- *            overlap the iterations: 1 = images >= 48 Mpx and >= 4096 rows
- *            (default), 0 = never, 2 = whenever engine and buffers allow.
+ *            overlap the iterations: 1 = when the hidden copies outweigh
+ *            the strips' extra launches (default; ~100 Mpx at 100
+ *            iterations), 0 = never, 2 = whenever engine and buffers allow.
  * Returns the previous value, or -1 for an unknown name. */
 int fdg_set_option(const char* name, int value);
 

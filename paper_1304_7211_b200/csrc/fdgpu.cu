@@ -1653,14 +1653,28 @@ std::vector<int> pipe_strips(int H, int D, int iters) {
     return a;
 }
 
-// option "pipeline": 0 off, 1 large images only (>= 48 Mpx, >= 4096 rows: the
-// strips must be tall enough to keep every SM busy), 2 whenever the engine and
-// the buffers allow (tests)
+// option "pipeline": 0 off, 1 when it pays (below), 2 whenever the engine and
+// the buffers allow (tests).
+// When it pays (measured, profiles/r02_pipeline_strip_tuning.txt): the
+// pipeline hides the copies (2 x 4 B/px at ~55 GB/s) but every strip beyond
+// the first adds one launch per iteration, each ~17 us dearer than its share
+// of a whole-image launch (35 row-times per CTA segment) -- more on short
+// strips, hence the factor 1.5 -- and ~3 ms of copies stay exposed.  100
+// iterations: 8192^2 loses 4 %, 10240^2 gains 5 %, 16384^2 gains 24 %; fewer
+// iterations move the break-even down, more move it up.
+bool pipe_pays(int W, int H, int iters, int shift) {
+    if (W < 2048 || H < 4096) return false;  // launches on strips must still fill the SMs
+    const int n = (int)pipe_strips(H, shift, iters).size();
+    const double copies = 2.0 * 4.0 * (double)W * H / 55e9;
+    const double extra = 1.5 * (n - 1) * (double)iters * 17e-6 + 3e-3;
+    return copies > extra;
+}
+
 bool pipe_applies(const fdg_solver* sv, int W, int H, int iters, const HostSrc& f, const HostDst& u_out) {
     const int mode = g_pipeline.load();
     if (mode < 1 || iters < 1 || sv->batch != 1) return false;
     if (!use_fused(sv->fwd.get()) || !fused_halo_ok(W) || use_rowres(sv->fwd.get(), W)) return false;
-    if (mode == 1 && ((long long)W * H < (48ll << 20) || H < 4096)) return false;
+    if (mode == 1 && !pipe_pays(W, H, iters, 2 * (sv->fwd->dev.my / 2))) return false;
     // in-place calls (the result over the input): downloads would land in
     // rows whose upload may still be queued
     const char *fa = static_cast<const char*>(f.base()), *ua = static_cast<const char*>(u_out.base());
