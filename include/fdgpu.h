@@ -124,12 +124,13 @@ int fdg_ctx_synchronize(fdg_ctx* ctx);
 /* number of kernel launches issued through this context so far */
 uint64_t fdg_ctx_launch_count(const fdg_ctx* ctx);
 /* Layout of the strip pipeline (no reference counterpart; host only): first
- * rows of the strips at iteration 0 for an image of `height` rows whose fused
- * iteration reaches `shift` rows up and down (2 x the box's vertical radius).
+ * rows of the strips at iteration 0 for a width x height image whose fused
+ * iteration reaches `shift` rows up and down (2 x the box's vertical radius),
+ * chosen by the library's timeline model of the call.
  * Strip s covers rows [bounds[s] - shift k, bounds[s + 1] - shift k) of
  * iteration k, clipped to the image (strip 0 from row 0, the last strip to the
  * last row).  Returns the number of strips. */
-int fdg_pipeline_layout(int height, int shift, int iterations, int* bounds, int cap);
+int fdg_pipeline_layout(int width, int height, int shift, int iterations, int* bounds, int cap);
 /* schedule of the context's last fdg_rl_deconvolve: 0 = upload, iterate,
  * download; n >= 2 = time-skewed pipeline over n row strips */
 int fdg_ctx_last_schedule(const fdg_ctx* ctx);

@@ -106,7 +106,7 @@ def lib():
             "fdg_ctx_synchronize": (C.c_int, [vp]),
             "fdg_ctx_launch_count": (C.c_uint64, [vp]),
             "fdg_ctx_last_schedule": (C.c_int, [vp]),
-            "fdg_pipeline_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_int]),
+            "fdg_pipeline_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_int]),
             "fdg_dispatch": (C.c_int, [D, C.c_int, ip]),
             "fdg_operator_accepts": (C.c_int, [C.c_int, D, ip]),
             "fdg_plan_create": (C.c_int, [vp, D, C.c_int, C.POINTER(vp)]),

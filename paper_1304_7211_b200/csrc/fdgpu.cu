@@ -1606,19 +1606,66 @@ struct PipeCache {
 void pipe_destroy(PipeCache* c) { delete c; }
 
 
+// Rows [lo, hi) of strip s at iteration k for boundaries a (clipped to the image)
+inline void pipe_range(const std::vector<int>& a, int H, int D, int s, int k, int* lo, int* hi) {
+    const int n = (int)a.size();
+    *lo = s == 0 ? 0 : std::min(H, std::max(0, a[s] - D * k));
+    *hi = s == n - 1 ? H : std::min(H, std::max(0, a[s + 1] - D * k));
+}
+
+// Timeline model of one pipelined call (seconds), from this round's
+// measurements on a B200 (profiles/r02_pipeline_*.txt): the fused kernel runs
+// whole 16384^2 iterations at ~290 Gpx/s, every launch costs ~17 us beyond its
+// share of that (35 row-times per CTA segment: halo rows + pipeline fill) and
+// up to 15 us more on short strips (below ~4000 rows of 16384 px the segments
+// get short), a launch never takes less than ~45 us (bands of 60 + 35 rows),
+// copies run at ~55 GB/s in each direction, uploads in strip order, downloads
+// in strip order after the strip's last launch.  Fitted on 22 measured
+// (size, iterations, layout) calls: mean error 1.6 %, worst 5 %.
+constexpr double PIPE_RATE = 290e9, PIPE_LAUNCH = 17e-6, PIPE_SHORT = 15e-6, PIPE_SHORT_ROWS = 4000.0,
+                 PIPE_MIN_LAUNCH = 45e-6, PIPE_COPY = 55e9;
+inline double pipe_launch_time(int rows, int W) {
+    const double re = (double)rows * W / 16384.0;  // rows of a 16384-wide image with the same pixels
+    return std::max(PIPE_MIN_LAUNCH, (double)rows * W / PIPE_RATE + PIPE_LAUNCH +
+                                         PIPE_SHORT * std::max(0.0, 1.0 - re / PIPE_SHORT_ROWS));
+}
+double pipe_model(const std::vector<int>& a, int W, int H, int D, int K) {
+    const int n = (int)a.size();
+    double up = 0.0, done = 0.0, dl = 0.0;
+    int c0 = 0;
+    for (int s = 0; s < n; ++s) {
+        const int c1 = s == n - 1 ? H : std::max(c0, std::min(H, a[s + 1] + D));
+        up += (double)(c1 - c0) * W * 4.0 / PIPE_COPY;
+        c0 = c1;
+        double t = std::max(done, up);
+        int lo = 0, hi = 0;
+        for (int k = 0; k < K; ++k) {
+            pipe_range(a, H, D, s, k, &lo, &hi);
+            if (hi > lo) t += pipe_launch_time(hi - lo, W);
+        }
+        done = t;
+        dl = std::max(dl, done) + (double)std::max(0, hi - lo) * W * 4.0 / PIPE_COPY;
+    }
+    return dl;
+}
+double plain_model(int W, int H, int K) {
+    return 2.0 * (double)W * H * 4.0 / PIPE_COPY + K * ((double)W * H / PIPE_RATE + PIPE_LAUNCH);
+}
+
 // Strip boundaries a_0 = 0 < a_1 < ... < a_{n-1} at iteration 0 (strip n - 1
 // always ends at row H - 1).  Short first strip (its upload is not hidden),
-// growing strips (the upload runs ~5x faster than the iterations, so it stays
-// ahead).  The last boundary may lie BELOW the image, a_{n-1} = H + D (k0 - 1):
-// clipped to H it makes the last strip empty until iteration k0, after which
-// it grows by D rows per iteration to D (K - k0) rows -- those are the rows
-// whose download nothing hides.  Measured on config 4
-// (profiles/r02_pipeline_strip_tuning.txt): a late tail saves 2 ms of short
-// launches but leaves the previous strip's 6 ms download with nothing to hide
-// behind, so the default is k0 = 0: a 64-row last strip from the start.
+// growing strips (at 100 iterations the upload runs ~5x faster than the
+// iterations, so it stays ahead), a last strip of 64 rows (it ends D (K - 1)
+// rows taller, and those download after the loop).  Every strip costs one
+// more launch per iteration, so the layout is chosen by the timeline model
+// among a few shapes (first strip 512 .. 3072 rows, growth x2 .. x6 up to a
+// cap, or one body strip).  The last boundary may lie BELOW the image,
+// a_{n-1} = H + D (k0 - 1): clipped to H it makes the last strip empty until
+// iteration k0 (FDG_PIPE_K0; measured, not the default: it leaves the
+// previous strip's download with nothing to hide behind).
 // FDG_PIPE_STRIPS="h0,h1,..." overrides the heights (the last strip takes the
-// rest), FDG_PIPE_K0 the birth iteration.
-std::vector<int> pipe_strips(int H, int D, int iters) {
+// rest).
+std::vector<int> pipe_strips(int H, int D, int iters, int W = 16384) {
     std::vector<int> a{0};
     const char* ek = getenv("FDG_PIPE_K0");
     const int k0 = ek ? atoi(ek) : 0;
@@ -1633,41 +1680,49 @@ std::vector<int> pipe_strips(int H, int D, int iters) {
         if (ek && late) a.push_back(H + D * (k0 - 1));
         return a;
     }
-    // Measured on config 4 (16384^2, 100 iterations, scripts/pipe_tune.sh):
-    // every strip costs ~2 ms of extra halo rows and pipeline fills over its
-    // 100 launches, so few strips.
     const int last = late ? 0 : std::min(64, std::max(4, H / 8));
     const int body = H - last;
-    int h = std::max(std::min(512, std::max(H / 4, 4 * D)), std::min(1024, H / 16));
-    const int cap = std::max(h, H * 3 / 8);
-    while (a.back() + h < body) {
-        a.push_back(a.back() + h);
-        h = std::min(cap, 4 * h);
+    auto finish = [&](std::vector<int> v) {
+        if (late)
+            v.push_back(H + D * (k0 - 1));
+        else if (body > v.back())
+            v.push_back(body);
+        return v;
+    };
+    std::vector<int> best;
+    double best_t = 0.0;
+    for (int first : {512, 1024, 1536, 2048, 3072}) {
+        const int h0 = std::max(std::min(first, std::max(H / 4, 4 * D)), 1);
+        for (int grow : {0, 2, 3, 4, 6}) {  // 0: one body strip after the first
+            std::vector<int> v{0};
+            int h = h0;
+            const int cap = std::max(h, H * 3 / 8);
+            while (v.back() + h < body) {
+                v.push_back(v.back() + h);
+                if (grow == 0) break;
+                h = std::min(cap, grow * h);
+            }
+            // fold a short remainder into the previous strip
+            if (v.size() > 2 && body - v.back() < (v.back() - v[v.size() - 2]) / 4) v.pop_back();
+            v = finish(v);
+            const double t = pipe_model(v, W, H, D, std::max(iters, 1));
+            if (best.empty() || t < best_t) {
+                best = v;
+                best_t = t;
+            }
+        }
     }
-    // fold a short remainder into the previous strip
-    if (a.size() > 2 && body - a.back() < (a.back() - a[a.size() - 2]) / 4) a.pop_back();
-    if (late)
-        a.push_back(H + D * (k0 - 1));
-    else if (body > a.back())
-        a.push_back(body);
-    return a;
+    return best;
 }
 
-// option "pipeline": 0 off, 1 when it pays (below), 2 whenever the engine and
-// the buffers allow (tests).
-// When it pays (measured, profiles/r02_pipeline_strip_tuning.txt): the
-// pipeline hides the copies (2 x 4 B/px at ~55 GB/s) but every strip beyond
-// the first adds one launch per iteration, each ~17 us dearer than its share
-// of a whole-image launch (35 row-times per CTA segment) -- more on short
-// strips, hence the factor 1.5 -- and ~3 ms of copies stay exposed.  100
-// iterations: 8192^2 loses 4 %, 10240^2 gains 5 %, 16384^2 gains 24 %; fewer
-// iterations move the break-even down, more move it up.
+// option "pipeline": 0 off, 1 when the timeline model says it pays, 2 whenever
+// the engine and the buffers allow (tests).  Measured at 100 iterations
+// (profiles/r02_pipeline_strip_tuning.txt): 16384^2 gains 24 %, 10240^2 5 %;
+// with fewer iterations much more (16384^2 x 30: 66 -> 41 ms).
 bool pipe_pays(int W, int H, int iters, int shift) {
-    if (W < 2048 || H < 4096) return false;  // launches on strips must still fill the SMs
-    const int n = (int)pipe_strips(H, shift, iters).size();
-    const double copies = 2.0 * 4.0 * (double)W * H / 55e9;
-    const double extra = 1.5 * (n - 1) * (double)iters * 17e-6 + 3e-3;
-    return copies > extra;
+    if (W < 2048 || H < 2048) return false;  // launches on strips must still fill the SMs
+    const std::vector<int> a = pipe_strips(H, shift, iters, W);
+    return pipe_model(a, W, H, shift, iters) < 0.97 * plain_model(W, H, iters);
 }
 
 bool pipe_applies(const fdg_solver* sv, int W, int H, int iters, const HostSrc& f, const HostDst& u_out) {
@@ -1688,7 +1743,7 @@ int rl_pipelined(fdg_ctx* ctx, fdg_solver* sv, const HostSrc& f, const HostDst& 
                  float* du, int pitch, std::vector<float>* mc, std::vector<int>* nf, std::vector<double>* sec) {
     const int W = sv->W, H = sv->H, K = sv->cfg.iterations;
     const int D = 2 * (sv->fwd->dev.my / 2);
-    const std::vector<int> a = pipe_strips(H, D, K);
+    const std::vector<int> a = pipe_strips(H, D, K, W);
     const int n = (int)a.size();  // strip s = [a_s, a_{s+1}) at iteration 0, the last one to the image's end
     ctx->last_schedule = n;
     if (!ctx->pipe) {
@@ -2033,15 +2088,15 @@ int fdg_rl_deconvolve(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_confi
     return rl_deconvolve_impl(ctx, desc, cfg, src, W, H, dst, trace);
 }
 
-// The strip pipeline's layout for an image of `height` rows, `shift` rows of
+// The strip pipeline's layout for a `width` x `height` image, `shift` rows of
 // dependency per iteration (2 x the box's vertical radius) and `iterations`
 // iterations: the strips' first rows at iteration 0 (bounds[0] = 0; a value
 // beyond height = a strip born later, see pipe_strips).  Returns the number of
 // strips (bounds holds min(n, cap) of them).  Host only: lets a test check the
 // schedule's dependences without a device.
-int fdg_pipeline_layout(int height, int shift, int iterations, int* bounds, int cap) {
-    if (height < 1 || shift < 0 || iterations < 0 || (cap > 0 && !bounds)) return 0;
-    const std::vector<int> a = pipe_strips(height, shift, iterations);
+int fdg_pipeline_layout(int width, int height, int shift, int iterations, int* bounds, int cap) {
+    if (width < 1 || height < 1 || shift < 0 || iterations < 0 || (cap > 0 && !bounds)) return 0;
+    const std::vector<int> a = pipe_strips(height, shift, iterations, width);
     for (int i = 0; i < (int)a.size() && i < cap; ++i) bounds[i] = a[i];
     return (int)a.size();
 }

@@ -18,9 +18,9 @@ import pytest
 from paper_1304_7211_b200._lib import lib
 
 
-def layout(height, shift, iters):
+def layout(height, shift, iters, width=16384):
     buf = (C.c_int * 64)()
-    n = lib().fdg_pipeline_layout(height, shift, iters, buf, 64)
+    n = lib().fdg_pipeline_layout(width, height, shift, iters, buf, 64)
     assert 1 <= n <= 64
     return [buf[i] for i in range(n)]
 
@@ -75,10 +75,17 @@ def test_library_layout_is_a_valid_schedule(height, shift, iters):
     replay(a, height, shift, iters)
 
 
-def test_config4_layout():
+def test_layouts_follow_the_timeline_model():
+    """Few strips when launches are dear relative to the copies (many
+    iterations, small images), more when the copies dominate."""
     os.environ.pop("FDG_PIPE_STRIPS", None)
     os.environ.pop("FDG_PIPE_K0", None)
-    assert layout(16384, 14, 100) == [0, 1024, 5120, 11264, 16320]
+    cfg4 = layout(16384, 14, 100)
+    assert cfg4[0] == 0 and cfg4[-1] == 16384 - 64 and 4 <= len(cfg4) <= 6
+    assert len(layout(8192, 14, 100, width=8192)) <= len(cfg4)
+    assert len(layout(16384, 14, 1000)) <= len(cfg4)
+    for w in (2048, 8192, 16384):
+        replay(layout(8192, 14, 40, width=w), 8192, 14, 40)
 
 
 @pytest.mark.parametrize("strips,k0", [("100,200,300", None), ("64,64,64,64", None), ("16,16", None),
