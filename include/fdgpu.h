@@ -95,8 +95,8 @@ int fdg_device_available(void);
 /* the calling thread's current CUDA device (FDG_ECUDA without a device) */
 int fdg_get_device(int* device);
 /* Process-wide engine options (no reference counterpart; tuning/testing):
- *   "fused": 1 = run each RL iteration of a centred odd square box (3x3 ..
- *            17x17; config 4 = 15x15) as one fused pass (kernels_fused.cu,
+ *   "fused": 1 = run each RL iteration of a centred odd box (extents 3 ..
+ *            17, square or not; config 4 = 15x15) as one fused pass (kernels_fused.cu,
  *            default), 0 = two fused-epilogue passes.
  *   "spans": GenericBox span-table kernels (kernels_spans.cu): 0 = by size
  *            (tile kernel up to 4.5 Mpx per launch, default), 1 = tile

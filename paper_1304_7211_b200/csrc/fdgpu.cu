@@ -594,7 +594,7 @@ int run_fused(fdg_ctx* ctx, const fdg_plan* pl, const float* u_in, const float* 
     if (yhi < 0) yhi = H - 1;
     cudaError_t r = launch_fused(u_in, f, u_out, pitch, W, y0, y1, ylo, yhi, batch, bstride, pl->dev.scale,
                                  (float)cfg->epsilon_div, cfg->clamp_nonnegative, mc, nf, te, st, halo_in, halo_out,
-                                 hp ? hp->pitch : 0, hp ? hp->stride : 0, 0, 0, 1, pl->dev.mx / 2);
+                                 hp ? hp->pitch : 0, hp ? hp->stride : 0, 0, 0, 1, pl->dev.mx / 2, pl->dev.my / 2);
     if (r != cudaSuccess) return cuda_err(r, "fused RL iteration launch");
     static const bool dbg = getenv("FDG_DEBUG_SYNC") != nullptr;  // diagnostics: fault at its launch
     if (dbg) {

@@ -171,7 +171,7 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
                          int yhi, int batch, long long bstride, float scale, float eps, int clamp,
                          unsigned* maxchange, int* nanflag, unsigned long long* tend, cudaStream_t st,
                          int halo_in = 0, int halo_out = 0, int pitch_h = 0, long long bstride_h = 0,
-                         int y2 = 0, int y3 = 0, int balanced = 1, int rx = 7);
+                         int y2 = 0, int y3 = 0, int balanced = 1, int rx = 7, int ry = 7);
 // The boundary bands of a row strip for the fused iteration (kernels_band.cu):
 // output rows [y0, y1) and [y2, y3) computed in place per 16 x 16 tile (no
 // row streaming), small enough to run next to the fused interior launch.

@@ -1,5 +1,5 @@
-// kernels_fused.cu -- one launch per Richardson-Lucy iteration for centred
-// square boxes 3 x 3 ... 17 x 17 (Box2d*, config 4 = 15 x 15): both
+// kernels_fused.cu -- one launch per Richardson-Lucy iteration for centred odd
+// boxes 3 x 3 ... 17 x 17, square or not (Box2d*, config 4 = 15 x 15): both
 // convolutions, the quotient and the multiplicative update fused, q never
 // leaving the SM.
 //
@@ -90,6 +90,7 @@ struct FusedArgs {
     unsigned long long* probe;  // diagnostics (FDG_FUSED_PROBE): per CTA {start, end, smid, rows}
     int halo_in;   // u_in carries FUSED_HALO_L / _R replicated columns left / right of every row
     int halo_out;  // write those columns of u_out too
+    int ry;        // vertical radius (read by the RY = 0 instantiations: any RY <= 8 at run time)
 };
 
 // ---- packed fp32x2 arithmetic (Blackwell FADD2 / FMUL2 / FFMA2)
@@ -171,35 +172,38 @@ __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
 
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 
-// vertical running sum over a ring of MY rows of float4 (one slot per thread)
-template <int MY>
+// vertical running sum over a ring of MY rows of float4 (one slot per thread);
+// MYT = 0: the ring height is a run-time value (rectangular boxes)
+template <int MYT>
 struct VRing {
     float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
     int n = 0, slot = 0;
+    int my_rt = 0;
+    __device__ __forceinline__ int my() const { return MYT ? MYT : my_rt; }
     // steady state: the ring is full
     __device__ __forceinline__ void push_full(float4* ring, int stride, int t, const float4 h) {
         float4* rs = ring + (size_t)slot * stride + t;
         const float4 o = *rs;
         col = add4(sub4(col, o), h);
         *rs = h;
-        slot = slot + 1 == MY ? 0 : slot + 1;
+        slot = slot + 1 == my() ? 0 : slot + 1;
     }
     __device__ __forceinline__ void refresh(const float4* ring, int stride, int t) {
         float4 fr = ring[t];
 #pragma unroll
-        for (int k = 1; k < MY; ++k) fr = add4(fr, ring[(size_t)k * stride + t]);
+        for (int k = 1; k < my(); ++k) fr = add4(fr, ring[(size_t)k * stride + t]);
         col = fr;
     }
     __device__ __forceinline__ void push(float4* ring, int stride, int t, const float4 h) {
-        if (n >= MY) {
+        if (n >= my()) {
             push_full(ring, stride, t, h);
         } else {
             col = add4(col, h);
             ring[(size_t)slot * stride + t] = h;
-            slot = slot + 1 == MY ? 0 : slot + 1;
+            slot = slot + 1 == my() ? 0 : slot + 1;
         }
         ++n;
-        if (n > MY && (n & (REFRESH - 1)) == 0) refresh(ring, stride, t);  // fp32 drift
+        if (n > my() && (n & (REFRESH - 1)) == 0) refresh(ring, stride, t);  // fp32 drift
     }
 };
 
@@ -213,7 +217,10 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     static_assert(G::OFF == 8 - RX, "window offset inside its chunk");
     constexpr int SS = S / R;
     constexpr int LAG = SS / 2;  // edge CTAs: the producer readies stage st - LAG
-    constexpr int MY = G::MY;
+    // RY = 0: the vertical radius comes with the arguments (rectangular boxes
+    // share one instantiation per RX); otherwise a compile-time constant
+    const int ry = RY ? RY : a.ry;
+    const int my = 2 * ry + 1;
     static_assert((QR & (QR - 1)) == 0, "q ring rows between the A and B warps: power of two");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -223,8 +230,8 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     uint64_t* qempty = qfull + QR;
     float* uring = reinterpret_cast<float*>(smem_raw + 512);
     float* qbuf = uring + S * G::USEG;                            // ring of QR q rows
-    float4* v1 = reinterpret_cast<float4*>(qbuf + QR * G::QSEG);  // MY x NT
-    float4* v2 = v1 + MY * NT;                                    // MY x NT
+    float4* v1 = reinterpret_cast<float4*>(qbuf + QR * G::QSEG);  // my x NT
+    float4* v2 = v1 + my * NT;                                    // my x NT
 
     const int tid = threadIdx.x;
 #ifdef FDG_FUSED_PROBE
@@ -237,10 +244,10 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
     // one column strip x0, output rows [yb0, yb1): fresh barriers, every role
     // runs its pipeline to the end of the segment
     auto run_segment = [&](const int x0, const int xown, const int yb0, const int yb1) {
-        const int qr_lo = max(a.ylo, yb0 - RY), qr_hi = min(a.yhi, yb1 - 1 + RY);
+        const int qr_lo = max(a.ylo, yb0 - ry), qr_hi = min(a.yhi, yb1 - 1 + ry);
         const int nq = qr_hi - qr_lo + 1;  // q rows this band needs
-        const int j0 = qr_lo - RY;         // first streamed u row (may be < 0: clamped)
-        const int steps = nq + 2 * RY;     // u rows streamed: j0 .. qr_hi + RY
+        const int j0 = qr_lo - ry;         // first streamed u row (may be < 0: clamped)
+        const int steps = nq + 2 * ry;     // u rows streamed: j0 .. qr_hi + RY
         const int useg0 = x0 - 2 * G::HX;  // image column of u-segment index 0
         // the u segment reaches outside the image: replicate columns 0 / W-1
         // there (not needed when u_in carries replicated halo columns)
@@ -292,8 +299,8 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
                         bulk_g2s(uring + (size_t)(s * R + r) * G::USEG + udst,
                                  a.u_in + img_u + (long long)clampi(j, a.ylo, a.yhi) * pitch_u + uc0, ubytes,
                                  &full[s]);
-                    if (j - RY >= qr_lo && j - RY <= qr_hi)
-                        l2_prefetch(a.f + img + (long long)(j - RY) * pitch + fc0, fbytes);
+                    if (j - ry >= qr_lo && j - ry <= qr_hi)
+                        l2_prefetch(a.f + img + (long long)(j - ry) * pitch + fc0, fbytes);
                 }
             };
             if (!prod_fix) {
@@ -383,11 +390,12 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
                 if (slowR)
                     for (int c = qc + 4; c < c0 + G::QW; ++c) qrow[c - c0] = vR;
             };
-            VRing<MY> r1;
+            VRing<RY ? 2 * RY + 1 : 0> r1;
+            r1.my_rt = my;
             int s = 0;
             unsigned phase = 0;
             // f for A(i): row j0 + i - RY (clamped: prefetches past the band are unused)
-            auto load_f = [&](int i) { return ldg4(fcol + clampi(j0 + i - RY, qr_lo, qr_hi) * pitch); };
+            auto load_f = [&](int i) { return ldg4(fcol + clampi(j0 + i - ry, qr_lo, qr_hi) * pitch); };
             // step i: u row j0 + i -> H1 -> vertical window -> q row i - 2 RY.
             // Steady (ST): ring full, a q row every step, the q slot was used
             // before, parity ODD known at compile time.
@@ -426,7 +434,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
                     r1.push_full(v1, NT, tid, h);
                 else
                     r1.push(v1, NT, tid, h);
-                const int r = i - 2 * RY;
+                const int r = i - 2 * ry;
                 if (ST || r >= 0) {
                     // f / max(v, eps): max.NaN keeps the reference's NaN propagation
                     const float4 q = quot4(r1.col, fx);
@@ -437,7 +445,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
                 if (!ST) fx = load_f(i + 2);
             };
             float4 F0 = load_f(0), F1 = load_f(1);
-            const int i_s = 2 * RY + QR;  // ring full, q rows past the first ring turn
+            const int i_s = 2 * ry + QR;  // ring full, q rows past the first ring turn
             // steady blocks end 2 rows before the last q row (prefetch stays in range)
             const int nblk = steps - 2 > i_s ? (steps - 2 - i_s) / REFRESH : 0;
             int i = 0;
@@ -446,7 +454,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
                 if (i + 1 < steps) step(std::false_type(), std::integral_constant<int, 1>(), i + 1, F1);
             }
             if (nblk) {
-                const float* fp = fcol + (long long)(j0 + i + 2 - RY) * pitch;  // f row of A(i + 2)
+                const float* fp = fcol + (long long)(j0 + i + 2 - ry) * pitch;  // f row of A(i + 2)
                 for (int b = 0; b < nblk; ++b) {
     #pragma unroll 1
                     for (int t = 0; t < REFRESH; t += 2, i += 2) {
@@ -473,7 +481,7 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
                         const float4 qb = quot4(r1.col, F1);
                         F0 = ldg4(fp);
                         F1 = ldg4(fp + pitch);
-                        const int r = i - 2 * RY;  // even: slots r, r + 1 in the same ring turn
+                        const int r = i - 2 * ry;  // even: slots r, r + 1 in the same ring turn
                         mbar_wait(&qempty[r & (QR - 1)], ((r / QR) - 1) & 1);
                         mbar_wait(&qempty[(r + 1) & (QR - 1)], (((r + 1) / QR) - 1) & 1);
                         put_q(qrow_ptr(r), qa);
@@ -517,7 +525,8 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         const int ocl = min(oc, a.Wp4 - 4);
         const float* ucol = a.u_in + img_u + ocl;
         float* ocol = a.u_out + img_o + oc;
-        VRing<MY> r2;
+        VRing<RY ? 2 * RY + 1 : 0> r2;
+        r2.my_rt = my;
         float4 hlast = make_float4(0.f, 0.f, 0.f, 0.f);
         float maxd = 0.f;
         const uint64_t pol_first = HINT ? policy_evict_first() : 0;
@@ -569,14 +578,14 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         };
         // pushes: q rows above the image replicate row 0 (extras), rows below
         // the image replicate the last one (trailing); output o = push - 2 RY
-        const int extras = qr_lo - (yb0 - RY);
+        const int extras = qr_lo - (yb0 - ry);
         const int band = yb1 - yb0;
         auto push_out = [&](const float4 h, float4 u) {
             r2.push(v2, NT, tb, h);
-            if (r2.n >= MY) store(std::false_type(), r2.n - MY, r2.col, u);
+            if (r2.n >= my) store(std::false_type(), r2.n - my, r2.col, u);
         };
         // warm-up: q rows 0 .. r_s-1 (ring not yet full)
-        const int r_s = (max(1, 2 * RY + 1 - extras) + 1) & ~1;
+        const int r_s = (max(1, 2 * ry + 1 - extras) + 1) & ~1;
         const int r_e = nq;  // steady: one push and one output per q row
         const int nblk = r_e > r_s ? (r_e - r_s) / REFRESH : 0;
         int r = 0;
@@ -584,19 +593,19 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
             hlast = take(r);
             if (r == 0)
                 for (int p = 0; p < extras; ++p) r2.push(v2, NT, tb, hlast);
-            const int o = r2.n + 1 - MY;
+            const int o = r2.n + 1 - my;
             push_out(hlast, o >= 0 ? load_u(o) : make_float4(0.f, 0.f, 0.f, 0.f));
         }
         if (nblk) {
             // here r2 is full and output o = r + extras - 2 RY follows every push
-            const int o0 = r + extras - 2 * RY;
+            const int o0 = r + extras - 2 * ry;
             float4 U0 = load_u(o0), U1 = load_u(o0 + 1);
             float4 U2 = PD > 2 ? load_u(o0 + 2) : U0, U3 = PD > 2 ? load_u(o0 + 3) : U1;
             auto blocks = [&](auto fs) {
                 for (int b = 0; b < nblk; ++b) {
     #pragma unroll 1
                     for (int t = 0; t < REFRESH; t += 2, r += 2) {
-                        const int o = r + extras - 2 * RY;
+                        const int o = r + extras - 2 * ry;
                         const float4 g0 = take(r);
                         const float4 g1 = take(r + 1);
                         r2.push_full(v2, NT, tb, g0);
@@ -625,9 +634,9 @@ __global__ void __launch_bounds__(2 * NT + 32, 2) k_fused(const FusedArgs a) {
         }
         for (; r < nq; ++r) {
             hlast = take(r);
-            push_out(hlast, load_u(r2.n + 1 - MY));
+            push_out(hlast, load_u(r2.n + 1 - my));
         }
-        while (r2.n - 2 * RY < band) push_out(hlast, load_u(r2.n + 1 - MY));  // below the image
+        while (r2.n - 2 * ry < band) push_out(hlast, load_u(r2.n + 1 - my));  // below the image
 
         if (a.maxchange) {
             const bool nan = isnan(maxd);
@@ -711,21 +720,24 @@ __global__ void k_pad_halo(const float* __restrict__ src, int pitch_src, long lo
 }
 
 template <int RX, int RY, int NT, int R, int S, int QR, int PD, bool HINT>
-size_t smem_bytes() {
+size_t smem_bytes(int my) {
     using G = FG<RX, RY, NT>;
-    return 512 + sizeof(float) * ((size_t)S * G::USEG + QR * (size_t)G::QSEG) + sizeof(float4) * 2 * (size_t)G::MY * NT;
+    return 512 + sizeof(float) * ((size_t)S * G::USEG + QR * (size_t)G::QSEG) + sizeof(float4) * 2 * (size_t)my * NT;
 }
 
 template <int RX, int RY, int NT, int R, int S, int QR, int PD, bool HINT>
 cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     using G = FG<RX, RY, NT>;
-    const size_t smem = smem_bytes<RX, RY, NT, R, S, QR, PD, HINT>();
+    const int ry = RY ? RY : a.ry, my = 2 * ry + 1;  // RY = 0: the radius is a run-time argument
+    if (ry < 1 || ry > 8) return cudaErrorInvalidValue;
+    a.ry = ry;
+    const size_t smem = smem_bytes<RX, RY, NT, R, S, QR, PD, HINT>(my);
     cudaError_t err = smem_attr<k_fused<RX, RY, NT, R, S, QR, PD, HINT>>();
     if (err != cudaSuccess) return err;
     static int occ = 0;
-    if (!occ) {
+    if (!occ) {  // (run-time radius: 17 rows, the tallest ring, still fits two CTAs per SM)
         err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused<RX, RY, NT, R, S, QR, PD, HINT>, 2 * NT + 32,
-                                                            smem);
+                                                            smem_bytes<RX, RY, NT, R, S, QR, PD, HINT>(RY ? my : 17));
         if (err != cudaSuccess) return err;
         if (occ < 1) occ = 1;
     }
@@ -741,7 +753,7 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     const long long per_wave = std::max(1LL, (long long)sms * occ / cols);
     const int rows = a.y1 - a.y0;
     if (rows <= 0) return cudaSuccess;
-    const long long ctas_y = std::min(per_wave, std::max(1LL, (long long)rows / (4 * G::MY)));
+    const long long ctas_y = std::min(per_wave, std::max(1LL, (long long)rows / (4 * my)));
     a.band = (int)((rows + ctas_y - 1) / ctas_y);
     if (const char* e = getenv("FDG_FUSED_BAND")) a.band = std::max(1, atoi(e));
     a.nb1 = (rows + a.band - 1) / a.band;
@@ -762,7 +774,7 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     if (lin_on && want_lin && rows2 <= 0 && a.batch == 1 && grid.x * grid.y < slots) {
         const long long total = (long long)strips * rows;
         const long long L = (total + slots - 1) / slots;
-        if (L >= 8 * G::MY) {
+        if (L >= 8 * my) {
             a.lin_len = (int)L;
             grid = dim3((unsigned)((total + L - 1) / L), 1, 1);
         }
@@ -803,10 +815,10 @@ std::atomic<int> g_fused{getenv("FDG_FUSED") ? atoi(getenv("FDG_FUSED")) : 1};
 void set_fused_mode(int v) { g_fused.store(v); }
 int fused_mode() { return g_fused.load(); }
 
-// centred square boxes 3 x 3 ... 17 x 17 (config 4 = 15 x 15)
+// centred odd boxes 3 x 3 ... 17 x 17, square or not (config 4 = 15 x 15)
 bool fused_supported(int mx, int my, int min_dx, int min_dy) {
-    return g_fused.load() == 1 && mx == my && (mx & 1) && mx >= 3 && mx <= 17 && min_dx == -(mx / 2) &&
-           min_dy == -(my / 2);
+    return g_fused.load() == 1 && (mx & 1) && (my & 1) && mx >= 3 && mx <= 17 && my >= 3 && my <= 17 &&
+           min_dx == -(mx / 2) && min_dy == -(my / 2);
 }
 
 int fused_halo_left() { return FUSED_HALO_L; }
@@ -824,7 +836,7 @@ cudaError_t launch_pad_halo(const float* src, int pitch_src, long long bs_src, f
 cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pitch, int W, int y0, int y1, int ylo,
                          int yhi, int batch, long long bstride, float scale, float eps, int clamp, unsigned* maxchange, int* nanflag,
                          unsigned long long* tend, cudaStream_t st, int halo_in, int halo_out, int pitch_h,
-                         long long bstride_h, int y2, int y3, int balanced, int rx) {
+                         long long bstride_h, int y2, int y3, int balanced, int rx, int ry) {
     FusedArgs a;
     a.lin_len = balanced ? 0 : -1;
     a.y2 = y2;
@@ -855,6 +867,20 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
     a.nanflag = nanflag;
     a.tend = tend;
     static const int variant = getenv("FDG_FUSED_V") ? atoi(getenv("FDG_FUSED_V")) : 0;
+    a.ry = ry;
+    if (rx != ry) {  // rectangular boxes: one instantiation per RX, the vertical radius at run time
+        switch (rx) {
+            case 1: return launch_t<1, 0, 128, 2, 12, 8, 2, true>(a, st);
+            case 2: return launch_t<2, 0, 128, 2, 12, 8, 2, true>(a, st);
+            case 3: return launch_t<3, 0, 128, 2, 12, 8, 2, true>(a, st);
+            case 4: return launch_t<4, 0, 128, 2, 12, 8, 2, true>(a, st);
+            case 5: return launch_t<5, 0, 128, 2, 12, 8, 2, true>(a, st);
+            case 6: return launch_t<6, 0, 128, 2, 12, 8, 2, true>(a, st);
+            case 7: return launch_t<7, 0, 128, 2, 12, 8, 2, true>(a, st);
+            case 8: return launch_t<8, 0, 128, 2, 12, 8, 2, true>(a, st);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (rx) {  // every radius but config 4's: the generic window sums (hsumx4)
         case 1: return launch_t<1, 1, 128, 2, 12, 8, 2, true>(a, st);  // 3 x 3
         case 2: return launch_t<2, 2, 128, 2, 12, 8, 2, true>(a, st);

@@ -181,7 +181,7 @@ int shard_init(fdg_shard* s, fdg_ctx* ctx, const fdg_psf_desc* psf, const fdg_rl
     if (st) return st;
     const DevPsf& d = s->fwd->dev;
     s->T = std::max(std::max(0, -d.min_dy), std::max(0, d.max_dy));
-    if (use_fused(s->fwd.get()) && fused_halo_ok(W) && d.mx == 15) {  // k_band: the 15 x 15 box
+    if (use_fused(s->fwd.get()) && fused_halo_ok(W) && d.mx == 15 && d.my == 15) {  // k_band: the 15 x 15 box
         s->engine = SH_FUSED;
         s->halo = 2 * s->T;
     } else if (use_rowres(s->fwd.get(), W)) {
@@ -298,7 +298,8 @@ int shard_fused(fdg_shard* s, int k, int y0, int y1, int y2, int y3, cudaStream_
     cudaError_t r = launch_fused(src, s->f, dst, s->pitch, s->W, y0, y1, shard_ylo(s), shard_yhi(s), 1, 0,
                                  s->fwd->dev.scale, (float)s->cfg.epsilon_div, s->cfg.clamp_nonnegative,
                                  s->mc.p + slot, s->nf.p + slot, s->ts.p + 1 + slot, st, k > 0, 1, s->hp.pitch,
-                                 s->hp.stride, y2, y3, s->world == 1 || s->core > 3000, s->fwd->dev.mx / 2);
+                                 s->hp.stride, y2, y3, s->world == 1 || s->core > 3000, s->fwd->dev.mx / 2,
+                                 s->fwd->dev.my / 2);
     if (r != cudaSuccess) return cuda_err(r, "fused RL iteration launch (strip)");
     s->ctx->launches += 1;
     return FDG_OK;

@@ -24,7 +24,16 @@ def rate(solver, f, u, it, reps=3):
 
 
 what = sys.argv[1] if len(sys.argv) > 1 else "boxes"
-if what == "boxes":
+if what == "rects":
+    n, it = 4096, 50
+    f = torch.rand(n, n, device='cuda') + 0.1
+    u = torch.empty_like(f)
+    for mx, my in ((15, 9), (9, 15), (17, 5), (5, 17), (7, 13)):
+        for fused in (0, 1):
+            lib().fdg_set_option(b"fused", fused)
+            s = RlSolver(makeBoxPsf(mx, my), RlConfig(iterations=it, op=K.Box2dSliding), n, n)
+            print(f"box {mx}x{my} 4096^2: engine {s.engine():6s} {rate(s, f, u, it):9.0f} Mpx*it/s")
+elif what == "boxes":
     n, it = 4096, 50
     f = torch.rand(n, n, device='cuda') + 0.1
     u = torch.empty_like(f)

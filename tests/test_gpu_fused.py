@@ -131,7 +131,7 @@ def test_fused_iterate_rejects_non_fused_solver():
     from paper_1304_7211_b200 import RlSolver
     from paper_1304_7211_b200._lib import FdgInvalidArgument
     from paper_1304_7211_b200.psf import makeBoxPsf
-    s = RlSolver(makeBoxPsf(5, 3), RlConfig(iterations=2, op=K.Box2dSliding), 64, 64)
+    s = RlSolver(makeBoxPsf(21, 3), RlConfig(iterations=2, op=K.Box2dSliding), 64, 64)
     assert s.engine() != "fused"
     with pytest.raises(FdgInvalidArgument):
         s.iterate(1, 2, 3, 64, 64 * 64, 0, 64, 0, 63, 0)
@@ -271,4 +271,24 @@ def test_rowres_every_line_length(m, w, h):
     res = rlDeconvolve(f, psf, RlConfig(iterations=9, op=K.Box1dSliding))
     ref, mc, _ = O.rl_deconvolve(f.astype(np.float64), psf, 9, O.BOX1D_SLIDING)
     assert W.max_rel(res.image, ref) <= 1e-5
+    np.testing.assert_allclose([r.maxAbsChange for r in res.trace.records], mc, rtol=1e-3, atol=1e-6)
+
+
+@pytest.mark.parametrize("mx,my", [(15, 9), (9, 15), (3, 17), (17, 3), (5, 7), (13, 11), (7, 15), (15, 3)])
+@pytest.mark.parametrize("w,h,it", [(1024, 768, 9), (37, 23, 5), (513, 129, 6), (2050, 300, 2), (600, 1, 3),
+                                    (8192, 20, 3)])
+def test_fused_rectangular_boxes_match_oracle(mx, my, w, h, it):
+    """Centred odd boxes with different extents: one instantiation per
+    horizontal radius, the vertical radius (ring height, halo rows) at run
+    time."""
+    from paper_1304_7211_b200 import RlSolver
+    from paper_1304_7211_b200.psf import makeBoxPsf
+    psf = makeBoxPsf(mx, my)
+    rng = np.random.default_rng(w * 7 + h + 31 * mx + my)
+    g = rng.uniform(0.05, 1.0, size=(h, w)).astype(np.float32)
+    f = np.maximum(W.blur_replicate(g, psf) + rng.normal(0, 0.01, size=g.shape), 1e-6).astype(np.float32)
+    assert RlSolver(psf, RlConfig(iterations=it, op=K.Box2dSliding), w, h).engine() == "fused"
+    res = rlDeconvolve(f, psf, RlConfig(iterations=it, op=K.Box2dSliding))
+    ref, mc, _ = O.rl_deconvolve(f.astype(np.float64), psf, it, O.BOX2D_SLIDING)
+    assert W.max_rel(res.image, ref) <= MAX_REL
     np.testing.assert_allclose([r.maxAbsChange for r in res.trace.records], mc, rtol=1e-3, atol=1e-6)

@@ -86,10 +86,10 @@ def test_pipelined_matches_oracle(w, h, it, strips):
     assert all(r.seconds > 0 for r in res.trace.records)
 
 
-@pytest.mark.parametrize("m", [3, 5, 9, 17])
-def test_pipelined_other_boxes(m):
-    psf = P.makeBoxPsf(m, m)
-    f, _ = _input(1024, 640, m, psf)
+@pytest.mark.parametrize("m,my", [(3, 3), (5, 5), (9, 9), (17, 17), (15, 9), (5, 13)])
+def test_pipelined_other_boxes(m, my):
+    psf = P.makeBoxPsf(m, my)  # the strips slide by 2 x the vertical radius
+    f, _ = _input(1024, 640, m + my, psf)
     out, _ = _run(f, psf, 15, "100,260")
     ref, _, _ = O.rl_deconvolve(f.astype(np.float64), psf, 15, O.BOX2D_SLIDING)
     assert W.max_rel(out, ref) <= MAX_REL
