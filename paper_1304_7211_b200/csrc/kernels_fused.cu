@@ -135,6 +135,8 @@ template <int RX>
 __device__ __forceinline__ float4 hsumx4(const float* seg, int chunk) {
     if constexpr (RX == 7) {
         return hsum15x4(seg, chunk);
+    } else if constexpr (RX == 0) {  // vertical lines: the window is the column itself
+        return reinterpret_cast<const float4*>(seg)[chunk + 2];
     } else {
         constexpr int OFF = 8 - RX, LAST = OFF + 3 + 2 * RX;
         constexpr int C0 = OFF / 4, C1 = LAST / 4;
@@ -815,9 +817,10 @@ std::atomic<int> g_fused{getenv("FDG_FUSED") ? atoi(getenv("FDG_FUSED")) : 1};
 void set_fused_mode(int v) { g_fused.store(v); }
 int fused_mode() { return g_fused.load(); }
 
-// centred odd boxes 3 x 3 ... 17 x 17, square or not (config 4 = 15 x 15)
+// centred odd boxes 3 x 3 ... 17 x 17, square or not (config 4 = 15 x 15), and
+// centred vertical lines of 3 ... 17 px
 bool fused_supported(int mx, int my, int min_dx, int min_dy) {
-    return g_fused.load() == 1 && (mx & 1) && (my & 1) && mx >= 3 && mx <= 17 && my >= 3 && my <= 17 &&
+    return g_fused.load() == 1 && (mx & 1) && (my & 1) && mx >= 1 && mx <= 17 && my >= 3 && my <= 17 &&
            min_dx == -(mx / 2) && min_dy == -(my / 2);
 }
 
@@ -870,6 +873,7 @@ cudaError_t launch_fused(const float* u_in, const float* f, float* u_out, int pi
     a.ry = ry;
     if (rx != ry) {  // rectangular boxes: one instantiation per RX, the vertical radius at run time
         switch (rx) {
+            case 0: return launch_t<0, 0, 128, 2, 12, 8, 2, true>(a, st);  // vertical lines
             case 1: return launch_t<1, 0, 128, 2, 12, 8, 2, true>(a, st);
             case 2: return launch_t<2, 0, 128, 2, 12, 8, 2, true>(a, st);
             case 3: return launch_t<3, 0, 128, 2, 12, 8, 2, true>(a, st);

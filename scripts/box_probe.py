@@ -28,7 +28,7 @@ if what == "rects":
     n, it = 4096, 50
     f = torch.rand(n, n, device='cuda') + 0.1
     u = torch.empty_like(f)
-    for mx, my in ((15, 9), (9, 15), (17, 5), (5, 17), (7, 13)):
+    for mx, my in ((15, 9), (9, 15), (17, 5), (5, 17), (7, 13), (1, 9), (1, 15)):
         for fused in (0, 1):
             lib().fdg_set_option(b"fused", fused)
             s = RlSolver(makeBoxPsf(mx, my), RlConfig(iterations=it, op=K.Box2dSliding), n, n)

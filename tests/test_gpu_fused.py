@@ -274,13 +274,14 @@ def test_rowres_every_line_length(m, w, h):
     np.testing.assert_allclose([r.maxAbsChange for r in res.trace.records], mc, rtol=1e-3, atol=1e-6)
 
 
-@pytest.mark.parametrize("mx,my", [(15, 9), (9, 15), (3, 17), (17, 3), (5, 7), (13, 11), (7, 15), (15, 3)])
+@pytest.mark.parametrize("mx,my", [(15, 9), (9, 15), (3, 17), (17, 3), (5, 7), (13, 11), (7, 15), (15, 3),
+                                   (1, 3), (1, 9), (1, 15), (1, 17)])
 @pytest.mark.parametrize("w,h,it", [(1024, 768, 9), (37, 23, 5), (513, 129, 6), (2050, 300, 2), (600, 1, 3),
                                     (8192, 20, 3)])
 def test_fused_rectangular_boxes_match_oracle(mx, my, w, h, it):
-    """Centred odd boxes with different extents: one instantiation per
-    horizontal radius, the vertical radius (ring height, halo rows) at run
-    time."""
+    """Centred odd boxes with different extents (and vertical lines, mx = 1):
+    one instantiation per horizontal radius, the vertical radius (ring height,
+    halo rows) at run time."""
     from paper_1304_7211_b200 import RlSolver
     from paper_1304_7211_b200.psf import makeBoxPsf
     psf = makeBoxPsf(mx, my)

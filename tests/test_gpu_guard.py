@@ -28,6 +28,7 @@ def _cases():
         ("fused 17x17 short", makeBoxPsf(17, 17), K.Box2dSliding, O.BOX2D_SLIDING, 640, 11, 3),
         ("fused 15x9", makeBoxPsf(15, 9), K.Box2dSliding, O.BOX2D_SLIDING, 1000, 150, 4),
         ("fused 3x17 ragged", makeBoxPsf(3, 17), K.Box2dSliding, O.BOX2D_SLIDING, 509, 60, 3),
+        ("fused vertical line 1x13", makeBoxPsf(1, 13), K.Box2dSliding, O.BOX2D_SLIDING, 640, 90, 4),
         ("box 31x3", makeBoxPsf(31, 3), K.Box2dSliding, O.BOX2D_SLIDING, 700, 130, 3),
         ("rowres line 15", makeLinePsf(15), K.Box1dSliding, O.BOX1D_SLIDING, 512, 96, 6),
         ("rowres line 31 ragged", makeLinePsf(31), K.Box1dSliding, O.BOX1D_SLIDING, 1022, 50, 4),
