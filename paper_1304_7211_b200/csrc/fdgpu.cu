@@ -574,9 +574,14 @@ int run_rowres(fdg_ctx* ctx, const fdg_plan* pl, const float* f, float* u, int p
 
 // Single-pass RL iteration (kernels_fused.cu) for the centred 15x15 box: the
 // forward and adjoint passes, quotient and update in one launch.
-bool use_fused(const fdg_plan* pl) {
+// px: pixels per launch (width x rows x batch) or < 0 for "does the box
+// qualify at all".  In mode 1 small launches stay on the two-pass path, whose
+// span-tile kernels (<= 0.5 Mpx, run_pass) beat the row-streaming fused kernel
+// there; mode 2 takes every qualifying box.
+bool use_fused(const fdg_plan* pl, long long px = -1) {
     const DevPsf& d = pl->dev;
-    return d.engine == ENG_RECT && fused_supported(d.mx, d.my, d.min_dx, d.min_dy);
+    if (d.engine != ENG_RECT || !fused_supported(d.mx, d.my, d.min_dx, d.min_dy)) return false;
+    return px < 0 || fused_mode() >= 2 || px > (512ll << 10);
 }
 
 // Haloed u planes of the fused loop (see launch_fused)
@@ -1375,7 +1380,8 @@ int solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long
     // columns, so no CTA handles image edges in its pipeline); the two-pass
     // engines use q
     static const bool no_halo = getenv("FDG_FUSED_NOHALO") != nullptr;
-    const bool fused_h = use_fused(s->fwd.get()) && fused_halo_ok(s->W) && !no_halo;
+    const long long launch_px = (long long)s->W * s->H * s->batch;
+    const bool fused_h = use_fused(s->fwd.get(), launch_px) && fused_halo_ok(s->W) && !no_halo;
     HaloPlanes hp;
     if (fused_h) {
         hp.pitch = (s->W + fused_halo_left() + fused_halo_right() + 31) & ~31;
@@ -1411,7 +1417,7 @@ int solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long long
         return FDG_OK;
     }
     const uint64_t before = ctx->launches;
-    const bool fused = !rowres && use_fused(s->fwd.get());
+    const bool fused = !rowres && use_fused(s->fwd.get(), launch_px);
     const TraceSlots tr = solver_slots(s);
     auto issue = [&]() -> int {
         cudaStream_t st = ctx->stream;
@@ -1728,7 +1734,7 @@ bool pipe_pays(int W, int H, int iters, int shift) {
 bool pipe_applies(const fdg_solver* sv, int W, int H, int iters, const HostSrc& f, const HostDst& u_out) {
     const int mode = g_pipeline.load();
     if (mode < 1 || iters < 1 || sv->batch != 1) return false;
-    if (!use_fused(sv->fwd.get()) || !fused_halo_ok(W) || use_rowres(sv->fwd.get(), W)) return false;
+    if (!use_fused(sv->fwd.get(), (long long)W * H) || !fused_halo_ok(W) || use_rowres(sv->fwd.get(), W)) return false;
     if (mode == 1 && !pipe_pays(W, H, iters, 2 * (sv->fwd->dev.my / 2))) return false;
     // in-place calls (the result over the input): downloads would land in
     // rows whose upload may still be queued
@@ -2023,7 +2029,7 @@ int rl_deconvolve_impl(fdg_ctx* ctx, const fdg_psf_desc* desc, const fdg_rl_conf
         CK(launch_stamp(tr.ts, s));
         ctx->launches += 1;
     }
-    const bool fused = !rowres && use_fused(fwd.get());
+    const bool fused = !rowres && use_fused(fwd.get(), (long long)W * H);
     for (int k = 0; fused && k < iters; ++k) {
         // ping-pong so the result lands in du: iteration k writes du when
         // (iters - 1 - k) is even; iteration 0 reads f itself (u0 = f)
@@ -2506,7 +2512,7 @@ int fdg_solver_run(fdg_solver* s, const float* d_f, float* d_u, int pitch, long 
 const char* fdg_solver_engine(const fdg_solver* s) {
     if (!s) return "?";
     if (use_rowres(s->fwd.get(), s->W)) return "rowres";
-    if (use_fused(s->fwd.get())) return "fused";
+    if (use_fused(s->fwd.get(), (long long)s->W * s->H * s->batch)) return "fused";
     return engine_name(s->fwd->dev.engine);
 }
 

@@ -755,7 +755,12 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     const long long per_wave = std::max(1LL, (long long)sms * occ / cols);
     const int rows = a.y1 - a.y0;
     if (rows <= 0) return cudaSuccess;
-    const long long ctas_y = std::min(per_wave, std::max(1LL, (long long)rows / (4 * my)));
+    // bands no shorter than the box (2 RY halo rows of q, 4 RY of u per band):
+    // short launches -- images up to ~2048^2, the pipeline's first and last
+    // strips -- need the CTAs more than the halo economy (2048^2 x 15 x 15:
+    // 43 -> 31.5 us per iteration against bands >= 4 MY; FDG_FUSED_MINBAND)
+    static const int minband = getenv("FDG_FUSED_MINBAND") ? std::max(1, atoi(getenv("FDG_FUSED_MINBAND"))) : 1;
+    const long long ctas_y = std::min(per_wave, std::max(1LL, (long long)rows / (minband * my)));
     a.band = (int)((rows + ctas_y - 1) / ctas_y);
     if (const char* e = getenv("FDG_FUSED_BAND")) a.band = std::max(1, atoi(e));
     a.nb1 = (rows + a.band - 1) / a.band;
@@ -808,8 +813,10 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     return e;
 }
 
-// Engine selection: 1 = on (default; beats the two-pass engine on config 4),
-// 0 = off; FDG_FUSED=0/1 or fdg_set_option("fused", v).
+// Engine selection: 1 = on where it pays (default: launches of more than 0.5
+// Mpx -- below that the two-pass span tiles win, 256^2 x 15 x 15: 8.6 vs 46 us
+// per iteration), 2 = whenever the box qualifies (tests), 0 = off;
+// FDG_FUSED=0/1/2 or fdg_set_option("fused", v).
 std::atomic<int> g_fused{getenv("FDG_FUSED") ? atoi(getenv("FDG_FUSED")) : 1};
 
 }  // namespace
@@ -820,7 +827,7 @@ int fused_mode() { return g_fused.load(); }
 // centred odd boxes 3 x 3 ... 17 x 17, square or not (config 4 = 15 x 15), and
 // centred vertical lines of 3 ... 17 px
 bool fused_supported(int mx, int my, int min_dx, int min_dy) {
-    return g_fused.load() == 1 && (mx & 1) && (my & 1) && mx >= 1 && mx <= 17 && my >= 3 && my <= 17 &&
+    return g_fused.load() >= 1 && (mx & 1) && (my & 1) && mx >= 1 && mx <= 17 && my >= 3 && my <= 17 &&
            min_dx == -(mx / 2) && min_dy == -(my / 2);
 }
 

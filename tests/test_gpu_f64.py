@@ -23,9 +23,11 @@ MAX_REL = 1e-4
 @pytest.fixture
 def forced_pipeline():
     prev = _lib.lib().fdg_set_option(b"pipeline", 2)
+    prev_f = _lib.lib().fdg_set_option(b"fused", 2)
     yield
     os.environ.pop("FDG_PIPE_STRIPS", None)
     _lib.lib().fdg_set_option(b"pipeline", prev)
+    _lib.lib().fdg_set_option(b"fused", prev_f)
 
 
 def _input64(w, h, seed, psf):

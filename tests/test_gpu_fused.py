@@ -18,7 +18,7 @@ MAX_REL = 1e-4
 @pytest.fixture(autouse=True)
 def fused_engine():
     from paper_1304_7211_b200._lib import lib
-    prev = lib().fdg_set_option(b"fused", 1)
+    prev = lib().fdg_set_option(b"fused", 2)  # every qualifying box, whatever the image size
     yield
     lib().fdg_set_option(b"fused", prev)
 
@@ -293,3 +293,25 @@ def test_fused_rectangular_boxes_match_oracle(mx, my, w, h, it):
     ref, mc, _ = O.rl_deconvolve(f.astype(np.float64), psf, it, O.BOX2D_SLIDING)
     assert W.max_rel(res.image, ref) <= MAX_REL
     np.testing.assert_allclose([r.maxAbsChange for r in res.trace.records], mc, rtol=1e-3, atol=1e-6)
+
+
+def test_fused_engine_is_chosen_by_launch_size():
+    """Option "fused" = 1 (the default): launches of up to 0.5 Mpx stay on the
+    two-pass path (its span-tile kernels win there), larger ones take the
+    one-launch iteration."""
+    from paper_1304_7211_b200 import RlSolver
+    from paper_1304_7211_b200._lib import lib
+    from paper_1304_7211_b200.psf import makeBoxPsf
+    prev = lib().fdg_set_option(b"fused", 1)
+    try:
+        cfg = RlConfig(iterations=3, op=K.Box2dSliding)
+        assert RlSolver(makeBoxPsf(15, 15), cfg, 512, 512).engine() != "fused"
+        assert RlSolver(makeBoxPsf(15, 15), cfg, 1024, 768).engine() == "fused"
+        assert RlSolver(makeBoxPsf(15, 15), cfg, 256, 256, batch=16).engine() == "fused"
+        f, psf = _input(640, 480, 5)
+        a = rlDeconvolve(f, psf, cfg).image
+        lib().fdg_set_option(b"fused", 2)
+        b = rlDeconvolve(f, psf, cfg).image
+        assert W.max_rel(a, b.astype(np.float64)) <= 1e-5
+    finally:
+        lib().fdg_set_option(b"fused", prev)

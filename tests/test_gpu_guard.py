@@ -20,6 +20,13 @@ pytestmark = pytest.mark.gpu
 GY = 9  # guard rows above / below
 
 
+@pytest.fixture(autouse=True)
+def every_qualifying_box_fused():
+    prev = lib().fdg_set_option(b"fused", 2)  # the fused kernel on these small planes too
+    yield
+    lib().fdg_set_option(b"fused", prev)
+
+
 def _cases():
     return [
         ("fused 15x15", makeBoxPsf(15, 15), K.Box2dSliding, O.BOX2D_SLIDING, 1024, 300, 5),

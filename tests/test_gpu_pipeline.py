@@ -25,7 +25,7 @@ MAX_REL = 1e-4
 
 @pytest.fixture(autouse=True)
 def forced_pipeline():
-    prev_f = _lib.lib().fdg_set_option(b"fused", 1)
+    prev_f = _lib.lib().fdg_set_option(b"fused", 2)
     prev = _lib.lib().fdg_set_option(b"pipeline", 2)
     old = os.environ.pop("FDG_PIPE_STRIPS", None)
     yield

@@ -91,7 +91,12 @@ def test_world1_shard_entry_point_host_and_device():
     assert sh.info["engine"] == "fused" and sh.info["exchanges_per_iteration"] == 0
     u = np.empty_like(f)
     tr = sh.run(f, u, trace=True)
-    single = rlDeconvolve(f, psf, cfg)
+    from paper_1304_7211_b200._lib import lib
+    prev = lib().fdg_set_option(b"fused", 2)  # the same engine for the 0.23 Mpx single-image run
+    try:
+        single = rlDeconvolve(f, psf, cfg)
+    finally:
+        lib().fdg_set_option(b"fused", prev)
     np.testing.assert_allclose(u, single.image, rtol=1e-6, atol=1e-7)
     assert len(tr) == 10 and all(r.seconds > 0 for r in tr)
     df = torch.from_numpy(f).cuda()
@@ -134,7 +139,12 @@ def test_world1_with_nccl_communicator():
     sh = ShardedRl(psf, cfg, w, h, 0, 1, comm_unique_id())
     u = np.empty_like(f)
     tr = sh.run(f, u, trace=True)
-    single = rlDeconvolve(f, psf, cfg)
+    from paper_1304_7211_b200._lib import lib
+    prev = lib().fdg_set_option(b"fused", 2)  # the same engine for the 0.23 Mpx single-image run
+    try:
+        single = rlDeconvolve(f, psf, cfg)
+    finally:
+        lib().fdg_set_option(b"fused", prev)
     np.testing.assert_allclose(u, single.image, rtol=1e-6, atol=1e-7)
     np.testing.assert_allclose([r.maxAbsChange for r in tr], [r.maxAbsChange for r in single.trace.records],
                                rtol=1e-5)
