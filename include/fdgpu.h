@@ -97,8 +97,9 @@ int fdg_get_device(int* device);
 /* Process-wide engine options (no reference counterpart; tuning/testing):
  *   "fused": 1 = run each RL iteration of a centred odd box (extents 3 ..
  *            17, square or not; config 4 = 15x15) as one fused pass
- *            (kernels_fused.cu) when a launch covers more than 0.5 Mpx
- *            (default), 2 = whatever the size, 0 = two fused-epilogue passes.
+ *            (kernels_fused.cu) when a launch is large enough for it to beat
+ *            the two passes (~3 Mpx; ~12 Mpx for boxes up to 9 px; default),
+ *            2 = whatever the size, 0 = two fused-epilogue passes.
  *   "spans": GenericBox span-table kernels (kernels_spans.cu): 0 = by size
  *            (tile kernel up to 4.5 Mpx per launch, default), 1 = tile
  *            kernel, 2 = marching kernel.

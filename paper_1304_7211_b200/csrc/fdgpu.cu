@@ -499,7 +499,14 @@ int run_pass(fdg_ctx* ctx, const fdg_plan* pl, const Geom& g, const Epi& e, cuda
     switch (d.engine) {
         case ENG_RECT:
             if (masked) return set_err(FDG_EINVAL, "operator does not support masked evaluation");
-            if (!g.wrap && (long long)g.W * (g.y1 - g.y0) * g.batch <= (512 << 10) && spans_jit_mode() &&
+            // boxes as span tables through the compiled tile kernel up to ~3072^2
+            // per launch: the row-streaming box engine is latency bound on
+            // small images (768^2 .. 2048^2 x 15 x 15: 53 us per RL iteration
+            // against 13 .. 37 us), draws level around 3072^2 and leads from
+            // 4096^2 (11 x 11: 159k vs 140k Mpx*it/s)
+            // (profiles/r02_engine_probe_4096.txt; FDG_BOX_TILE_PX)
+            static const long long tile_px = getenv("FDG_BOX_TILE_PX") ? atoll(getenv("FDG_BOX_TILE_PX")) : (10ll << 20);
+            if (!g.wrap && (long long)g.W * (g.y1 - g.y0) * g.batch <= tile_px && spans_jit_mode() &&
                 spans_jit_ready(d)) {
                 r = launch_spans_jit(d, g, e, st);
                 if (r != cudaErrorNotSupported) break;
@@ -576,12 +583,16 @@ int run_rowres(fdg_ctx* ctx, const fdg_plan* pl, const float* f, float* u, int p
 // forward and adjoint passes, quotient and update in one launch.
 // px: pixels per launch (width x rows x batch) or < 0 for "does the box
 // qualify at all".  In mode 1 small launches stay on the two-pass path, whose
-// span-tile kernels (<= 0.5 Mpx, run_pass) beat the row-streaming fused kernel
-// there; mode 2 takes every qualifying box.
+// span-tile kernels (run_pass) beat the row-streaming fused kernel there:
+// measured crossovers (profiles/r02_engine_probe_4096.txt) ~3 Mpx for boxes of
+// 11 px and more (1536^2: level, 2048^2: fused 31 vs 37 us per iteration),
+// ~12 Mpx for smaller ones (3072^2 x 5x5: 50.5 vs 47.6, 4096^2: 67 vs 80).
+// Mode 2 takes every qualifying box.
 bool use_fused(const fdg_plan* pl, long long px = -1) {
     const DevPsf& d = pl->dev;
     if (d.engine != ENG_RECT || !fused_supported(d.mx, d.my, d.min_dx, d.min_dy)) return false;
-    return px < 0 || fused_mode() >= 2 || px > (512ll << 10);
+    if (px < 0 || fused_mode() >= 2) return true;
+    return px > (std::max(d.mx, d.my) <= 9 ? (12ll << 20) : (3ll << 20));
 }
 
 // Haloed u planes of the fused loop (see launch_fused)

@@ -813,9 +813,9 @@ cudaError_t launch_t(FusedArgs a, cudaStream_t st) {
     return e;
 }
 
-// Engine selection: 1 = on where it pays (default: launches of more than 0.5
-// Mpx -- below that the two-pass span tiles win, 256^2 x 15 x 15: 8.6 vs 46 us
-// per iteration), 2 = whenever the box qualifies (tests), 0 = off;
+// Engine selection: 1 = on where it pays (default: launches of more than ~3
+// Mpx, ~12 Mpx for boxes up to 9 px -- below that the two-pass span tiles win,
+// use_fused in fdgpu.cu), 2 = whenever the box qualifies (tests), 0 = off;
 // FDG_FUSED=0/1/2 or fdg_set_option("fused", v).
 std::atomic<int> g_fused{getenv("FDG_FUSED") ? atoi(getenv("FDG_FUSED")) : 1};
 

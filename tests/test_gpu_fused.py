@@ -296,9 +296,9 @@ def test_fused_rectangular_boxes_match_oracle(mx, my, w, h, it):
 
 
 def test_fused_engine_is_chosen_by_launch_size():
-    """Option "fused" = 1 (the default): launches of up to 0.5 Mpx stay on the
-    two-pass path (its span-tile kernels win there), larger ones take the
-    one-launch iteration."""
+    """Option "fused" = 1 (the default): small launches stay on the two-pass
+    path (its span-tile kernels win there: up to ~3 Mpx, ~12 Mpx for boxes of
+    at most 9 px), larger ones take the one-launch iteration."""
     from paper_1304_7211_b200 import RlSolver
     from paper_1304_7211_b200._lib import lib
     from paper_1304_7211_b200.psf import makeBoxPsf
@@ -306,8 +306,11 @@ def test_fused_engine_is_chosen_by_launch_size():
     try:
         cfg = RlConfig(iterations=3, op=K.Box2dSliding)
         assert RlSolver(makeBoxPsf(15, 15), cfg, 512, 512).engine() != "fused"
-        assert RlSolver(makeBoxPsf(15, 15), cfg, 1024, 768).engine() == "fused"
-        assert RlSolver(makeBoxPsf(15, 15), cfg, 256, 256, batch=16).engine() == "fused"
+        assert RlSolver(makeBoxPsf(15, 15), cfg, 1536, 1536).engine() != "fused"
+        assert RlSolver(makeBoxPsf(15, 15), cfg, 2048, 2048).engine() == "fused"
+        assert RlSolver(makeBoxPsf(15, 15), cfg, 256, 256, batch=64).engine() == "fused"
+        assert RlSolver(makeBoxPsf(5, 5), cfg, 3072, 3072).engine() != "fused"
+        assert RlSolver(makeBoxPsf(5, 5), cfg, 4096, 4096).engine() == "fused"
         f, psf = _input(640, 480, 5)
         a = rlDeconvolve(f, psf, cfg).image
         lib().fdg_set_option(b"fused", 2)
