@@ -639,6 +639,15 @@ cudaError_t launch_tile(const SpanArgs& a, const Geom& g, const Epi& e, cudaStre
     return cudaErrorInvalidValue;
 }
 
+// Largest launch (pixels) the tile kernel takes before the marching kernel
+// does.  Measured per RL iteration (profiles/r02_engine_probe_4096.txt): the
+// disc's tiles lead at every size tried (4096^2: 140 vs 173 us, 6144^2: 280 vs
+// 331), the oblique line's up to 2560^2 (43 vs 54 us; 3072^2: 67 vs 54).
+template <class SH>
+constexpr long long tile_limit() {
+    return SH::NR > 16 ? (128ll << 20) : (7ll << 20);
+}
+
 template <class SH>
 cudaError_t launch_shape(const DevPsf& p, const Geom& g, const Epi& e, cudaStream_t st) {
     SpanArgs a;
@@ -661,12 +670,12 @@ cudaError_t launch_shape(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
     a.tend = e.tend;
     static const int nt_env = env_int("FDG_SPANS_NT");
     static const int g_env = env_int("FDG_SPANS_G");
-    // Small images (<= 4.5 Mpx per launch): the tile kernel -- the marching
-    // grid cannot fill the SMs (profiles/r01_spans_notes.md); larger ones
-    // march.  fdg_set_option("spans", 1 | 2) forces one (tests, A/B).
+    // Small images: the tile kernel -- the marching grid cannot fill the SMs
+    // (profiles/r01_spans_notes.md); larger ones march (tile_limit).
+    // fdg_set_option("spans", 1 | 2) forces one (tests, A/B).
     const long long px = (long long)g.W * (g.y1 - g.y0) * g.batch;
     const int mode = spans_mode();
-    const bool tile = mode ? mode == 1 : px <= 4608ll * 1024;
+    const bool tile = mode ? mode == 1 : px <= tile_limit<SH>();
     if (tile) {
         // disc: 128 x 56 tiles, 64 registers forced (4 CTAs = 32 warps per SM;
         // the register count of this kernel otherwise drifts between builds,
@@ -718,7 +727,8 @@ cudaError_t launch_spans(const DevPsf& p, const Geom& g, const Epi& e, cudaStrea
 const char* spans_kernel(const DevPsf& p, long long px) {
     if (spans_mode() != 3 && (same_shape<DiscR10>(p) || same_shape<Oblique21>(p))) {
         const int mode = spans_mode();
-        return (mode ? mode == 1 : px <= 4608ll * 1024) ? "tile" : "marching";
+        const long long lim = same_shape<DiscR10>(p) ? tile_limit<DiscR10>() : tile_limit<Oblique21>();
+        return (mode ? mode == 1 : px <= lim) ? "tile" : "marching";
     }
     if (spans_mode() != 3 && spans_jit_mode() && spans_jit_ready(p)) return "jit-tile";
     return "runtime-table";
